@@ -1,0 +1,811 @@
+// nnca.cu — NNCA construction on the GPU (compress.py:216 select_pivots,
+// compress.py:285 assemble) with the partially pivoted ACA of
+// _accel/_core.pyx:184 run as one CTA per cell, level-batched bottom-up.
+//
+// Pivot parity: every residual entry is formed with the reference's exact
+// operation order (kernel value, then `acc -= U[i,t] * V[j,t]` for t =
+// 0..k-1, no FMA), so residual rows/columns are bitwise identical to the
+// reference's and the argmax pivot choices (ties -> lowest index) agree.
+// Only the Frobenius-norm bookkeeping for the stopping test is a parallel
+// reduction (different summation order), which can flip the stop decision
+// only when ||u_k|| ||v_k|| lands within roundoff of eps ||A_k||_F.
+//
+// Interpolation operators (aca.py:476 row_interpolator, :490
+// col_interpolator) are back-substitutions against the pivot rows of U / V
+// — the ACA byproduct, no further kernel evaluations (paper Remark 2).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+
+#include "engine.cuh"
+
+namespace h2b {
+
+namespace {
+
+constexpr int ACA_THREADS = 256;
+constexpr int ACA_WARPS = ACA_THREADS / 32;
+
+struct AcaArgs {
+  int kind;
+  double a, eps2;
+  int64_t cell0;
+  const int64_t *m, *n, *cap;
+  const double* row_base;
+  int64_t ld_row;
+  const int64_t* row_off;
+  const int64_t* row_gidx;
+  const double* col_base;
+  int64_t ld_col;
+  const int64_t* col_off;
+  const int64_t* col_gidx;
+  double* U;
+  const int64_t* u_off;
+  double* V;
+  const int64_t* v_off;
+  unsigned char* flags;
+  const int64_t* f_off;
+  const int64_t* piv_off;
+  int64_t *rp, *cp;        // local pivots (staging, at piv_off)
+  int64_t *tpiv, *spiv;    // global pivot indices (staging, at piv_off)
+  int64_t *rank, *conv, *nevals;
+};
+
+struct RedScratch {
+  double v[ACA_WARPS];
+  long long i[ACA_WARPS];
+};
+
+__device__ void block_argmax(double& v, int64_t& i, RedScratch& rs) {
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  warp_argmax(v, i);
+  __syncthreads();
+  if (lane == 0) {
+    rs.v[w] = v;
+    rs.i[w] = i;
+  }
+  __syncthreads();
+  v = -1.0;
+  i = -1;
+  for (int q = 0; q < ACA_WARPS; q++) argmax_merge(v, i, rs.v[q], rs.i[q]);
+}
+
+__device__ double block_sum(double x, RedScratch& rs) {
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  x = warp_sum(x);
+  __syncthreads();
+  if (lane == 0) rs.v[w] = x;
+  __syncthreads();
+  double s = 0.0;
+  for (int q = 0; q < ACA_WARPS; q++) s += rs.v[q];
+  return s;
+}
+
+__device__ int64_t block_min(int64_t x, RedScratch& rs) {
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  x = warp_min_i64(x);
+  __syncthreads();
+  if (lane == 0) rs.i[w] = x;
+  __syncthreads();
+  int64_t s = INT64_MAX;
+  for (int q = 0; q < ACA_WARPS; q++) s = rs.i[q] < s ? rs.i[q] : s;
+  return s;
+}
+
+// _core.pyx:184-305, one CTA per cell
+template <int D>
+__global__ void __launch_bounds__(ACA_THREADS) aca_kernel(AcaArgs A) {
+  extern __shared__ double sm[];
+  __shared__ RedScratch rs;
+  __shared__ double xt[D], yb[D];
+  const int64_t cell = A.cell0 + blockIdx.x;
+  const int64_t m = A.m[cell], n = A.n[cell], cap = A.cap[cell];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (m == 0 || n == 0 || cap == 0) {
+    if (tid == 0) {
+      A.rank[cell] = 0;
+      A.conv[cell] = (m == 0 || n == 0) ? 1 : 0;
+      A.nevals[cell] = 0;
+    }
+    return;
+  }
+  double* urow = sm;
+  double* vcol = sm + cap;
+  double* crossv = sm + 2 * cap;
+  double* crossu = sm + 3 * cap;
+  const double* Xb = A.row_base + A.row_off[cell];
+  const double* Yb = A.col_base + A.col_off[cell];
+  const int64_t ldr = A.ld_row, ldc = A.ld_col;
+  double* U = A.U + A.u_off[cell];
+  double* V = A.V + A.v_off[cell];
+  unsigned char* ru = A.flags + A.f_off[cell];
+  unsigned char* cu = ru + m;
+  int64_t* rp = A.rp + A.piv_off[cell];
+  int64_t* cp = A.cp + A.piv_off[cell];
+  for (int64_t q = tid; q < m + n; q += ACA_THREADS) ru[q] = 0;
+  const int64_t full = m < n ? m : n;
+  int64_t k = 0, trial = 0, nev = 0;
+  double norm2 = 0.0;
+  int64_t converged = 1;
+  __syncthreads();
+  for (;;) {
+    bool exhausted = false;
+    double best;
+    int64_t bj;
+    for (;;) {
+      if (tid == 0) ru[trial] = 1;
+      for (int64_t t = tid; t < k; t += ACA_THREADS) urow[t] = U[t * m + trial];
+      if (tid < D) xt[tid] = Xb[tid * ldr + trial];
+      __syncthreads();
+      double xl[D];
+#pragma unroll
+      for (int q = 0; q < D; q++) xl[q] = xt[q];
+      best = -1.0;
+      bj = -1;
+      for (int64_t j = tid; j < n; j += ACA_THREADS) {
+        double yl[D];
+#pragma unroll
+        for (int q = 0; q < D; q++) yl[q] = Yb[q * ldc + j];
+        double acc = kval_exact(A.kind, A.a, r2_exact<D>(xl, yl));
+        const double* Vj = V + j;
+        for (int64_t t = 0; t < k; t++) acc = __dsub_rn(acc, __dmul_rn(urow[t], Vj[t * n]));
+        V[k * n + j] = acc;
+        if (!cu[j]) {
+          double val = fabs(acc);
+          if (val > best) {
+            best = val;
+            bj = j;
+          }
+        }
+      }
+      if (bj < 0) best = -1.0;
+      block_argmax(best, bj, rs);
+      nev += n;
+      if (best > 0.0) break;
+      int64_t first = INT64_MAX;
+      for (int64_t i = tid; i < m; i += ACA_THREADS)
+        if (!ru[i] && i < first) first = i;
+      first = block_min(first, rs);
+      if (first == INT64_MAX) {
+        exhausted = true;
+        break;
+      }
+      trial = first;
+      __syncthreads();
+    }
+    if (exhausted) break;
+    const double piv = V[k * n + bj];
+    double v2p = 0.0;
+    for (int64_t j = tid; j < n; j += ACA_THREADS) {
+      double v = __ddiv_rn(V[k * n + j], piv);
+      V[k * n + j] = v;
+      v2p += v * v;
+    }
+    if (tid < D) yb[tid] = Yb[tid * ldc + bj];
+    __syncthreads();
+    if (tid == 0) cu[bj] = 1;
+    for (int64_t t = tid; t < k; t += ACA_THREADS) vcol[t] = V[t * n + bj];
+    for (int64_t t = warp; t < k; t += ACA_WARPS) {
+      double s = 0.0;
+      const double* Vt = V + t * n;
+      const double* Vk = V + k * n;
+      for (int64_t j = lane; j < n; j += 32) s += Vt[j] * Vk[j];
+      s = warp_sum(s);
+      if (lane == 0) crossv[t] = s;
+    }
+    __syncthreads();
+    double yl[D];
+#pragma unroll
+    for (int q = 0; q < D; q++) yl[q] = yb[q];
+    double u2p = 0.0;
+    for (int64_t i = tid; i < m; i += ACA_THREADS) {
+      double xl[D];
+#pragma unroll
+      for (int q = 0; q < D; q++) xl[q] = Xb[q * ldr + i];
+      double acc = kval_exact(A.kind, A.a, r2_exact<D>(xl, yl));
+      for (int64_t t = 0; t < k; t++) acc = __dsub_rn(acc, __dmul_rn(U[t * m + i], vcol[t]));
+      U[k * m + i] = acc;
+      u2p += acc * acc;
+    }
+    nev += m;
+    __syncthreads();
+    for (int64_t t = warp; t < k; t += ACA_WARPS) {
+      double s = 0.0;
+      const double* Ut = U + t * m;
+      const double* Uk = U + k * m;
+      for (int64_t i = lane; i < m; i += 32) s += Ut[i] * Uk[i];
+      s = warp_sum(s);
+      if (lane == 0) crossu[t] = s;
+    }
+    double u2 = block_sum(u2p, rs);
+    double v2 = block_sum(v2p, rs);  // block_sum syncs: crossu/crossv visible
+    for (int64_t t = 0; t < k; t++) norm2 += 2.0 * crossu[t] * crossv[t];
+    norm2 += u2 * v2;
+    if (tid == 0) {
+      rp[k] = trial;
+      cp[k] = bj;
+    }
+    k += 1;
+    int stop = 0;
+    if (u2 * v2 <= A.eps2 * (norm2 > 0.0 ? norm2 : 0.0)) stop = 1;
+    else if (k == full) stop = 1;
+    else if (k == cap) stop = 2;
+    if (stop) {
+      if (stop == 2) converged = 0;
+      break;
+    }
+    best = -1.0;
+    int64_t bi = -1;
+    const double* Uk = U + (k - 1) * m;
+    for (int64_t i = tid; i < m; i += ACA_THREADS)
+      if (!ru[i]) {
+        double val = fabs(Uk[i]);
+        if (val > best) {
+          best = val;
+          bi = i;
+        }
+      }
+    block_argmax(best, bi, rs);
+    if (bi < 0) break;
+    trial = bi;
+    __syncthreads();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    A.rank[cell] = k;
+    A.conv[cell] = converged;
+    A.nevals[cell] = nev;
+  }
+  for (int64_t t = tid; t < k; t += ACA_THREADS) {
+    A.tpiv[A.piv_off[cell] + t] = A.row_gidx ? A.row_gidx[A.row_off[cell] + rp[t]] : rp[t];
+    A.spiv[A.piv_off[cell] + t] = A.col_gidx ? A.col_gidx[A.col_off[cell] + cp[t]] : cp[t];
+  }
+}
+
+// aca.py:476 row_interpolator: P = U L^{-1}, L[t][s] = U[rp[t], s]; P[rp] = I.
+// which==1: aca.py:490 col_interpolator: Q = V R^{-T}, R unit upper, Q[cp] = I.
+__global__ void interp_kernel(int which, int64_t cell0, const int64_t* __restrict__ rows_of,
+                              const int64_t* __restrict__ rank, const double* __restrict__ W,
+                              const int64_t* __restrict__ w_off, const int64_t* __restrict__ piv_loc,
+                              const int64_t* __restrict__ piv_off, double* __restrict__ out,
+                              const int64_t* __restrict__ out_off) {
+  const int64_t cell = cell0 + blockIdx.x;
+  const int64_t m = rows_of[cell], k = rank[cell];
+  if (k == 0 || m == 0) return;
+  const double* F = W + w_off[cell];
+  const int64_t* pv = piv_loc + piv_off[cell];
+  double* P = out + out_off[cell];
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    for (int64_t s = k - 1; s >= 0; s--) {
+      const double* Fs = F + s * m;
+      double acc = Fs[i];
+      for (int64_t t = s + 1; t < k; t++) acc -= P[t * m + i] * Fs[pv[t]];
+      P[s * m + i] = which == 0 ? acc / Fs[pv[s]] : acc;
+    }
+  }
+  __syncthreads();
+  for (int64_t q = threadIdx.x; q < k * k; q += blockDim.x) {
+    int64_t t = q / k, s = q % k;
+    P[s * m + pv[t]] = (s == t) ? 1.0 : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------
+// candidate set sizing / gathering (compress.py:159 candidate_sets)
+// ---------------------------------------------------------------------
+struct Src {
+  const double* coords;  // SoA, ld
+  int64_t ld;
+  const int64_t* gidx;   // global index per position
+  const int64_t* ptr;    // per cell of the "owner" level: range via ptr[range_lo[c]] .. ptr[range_hi[c]]
+  const int64_t* lo_map; // maps cell c -> index into ptr for begin (identity at leaf; ch_ptr otherwise)
+};
+
+// range of positions of cell c in the source: [ptr[map(c)], ptr[map(c+1)])
+__device__ __forceinline__ void src_range(const Src& S, int64_t c, int64_t& b, int64_t& e) {
+  if (S.lo_map) {
+    b = S.ptr[S.lo_map[c]];
+    e = S.ptr[S.lo_map[c + 1]];
+  } else {
+    b = S.ptr[c];
+    e = S.ptr[c + 1];
+  }
+}
+
+__global__ void cand_sizes(int64_t n, Src own, Src far, const int64_t* __restrict__ il_ptr,
+                           const int64_t* __restrict__ il_idx, int64_t* own_b, int64_t* own_len,
+                           int64_t* far_len) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  int64_t b, e;
+  src_range(own, c, b, e);
+  own_b[c] = b;
+  own_len[c] = e - b;
+  int64_t tot = 0;
+  for (int64_t q = il_ptr[c]; q < il_ptr[c + 1]; q++) {
+    src_range(far, il_idx[q], b, e);
+    tot += e - b;
+  }
+  far_len[c] = tot;
+}
+
+// concatenate the far-field source ranges of each cell (IL order) into a
+// contiguous SoA buffer (ld = total) with their global indices
+template <int D>
+__global__ void gather_far(int64_t cell0, Src far, const int64_t* __restrict__ il_ptr,
+                           const int64_t* __restrict__ il_idx, const int64_t* __restrict__ dst_off,
+                           double* __restrict__ dst, int64_t ld_dst, int64_t* __restrict__ dst_gidx) {
+  const int64_t cell = cell0 + blockIdx.x;
+  int64_t w = dst_off[cell];
+  for (int64_t q = il_ptr[cell]; q < il_ptr[cell + 1]; q++) {
+    int64_t b, e;
+    src_range(far, il_idx[q], b, e);
+    for (int64_t p = b + threadIdx.x; p < e; p += blockDim.x) {
+      int64_t o = w + (p - b);
+#pragma unroll
+      for (int k = 0; k < D; k++) dst[k * ld_dst + o] = far.coords[k * far.ld + p];
+      dst_gidx[o] = far.gidx[p];
+    }
+    w += e - b;
+  }
+}
+
+template <int D>
+__global__ void gather_coords(const double* __restrict__ aos, const int64_t* __restrict__ gidx, int64_t n,
+                              double* __restrict__ soa) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t g = gidx[i];
+#pragma unroll
+  for (int k = 0; k < D; k++) soa[k * n + i] = aos[g * D + k];
+}
+
+__global__ void compact_pivots(int64_t n, const int64_t* __restrict__ rank, const int64_t* __restrict__ piv_off,
+                               const int64_t* __restrict__ ptr, const int64_t* __restrict__ tp,
+                               const int64_t* __restrict__ sp, int64_t* __restrict__ t_out,
+                               int64_t* __restrict__ s_out) {
+  int64_t c = blockIdx.x;
+  if (c >= n) return;
+  for (int64_t t = threadIdx.x; t < rank[c]; t += blockDim.x) {
+    t_out[ptr[c] + t] = tp[piv_off[c] + t];
+    s_out[ptr[c] + t] = sp[piv_off[c] + t];
+  }
+}
+
+// compress.py:307-328 entry counts: sum_B kin(B) * sum_{C in IL(B)} kout(C)
+__global__ void coupling_counts(int64_t n, const int64_t* __restrict__ kin, const int64_t* __restrict__ kout,
+                                const int64_t* __restrict__ il_ptr, const int64_t* __restrict__ il_idx,
+                                unsigned long long* out) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n || kin[c] == 0) return;
+  int64_t s = 0;
+  for (int64_t q = il_ptr[c]; q < il_ptr[c + 1]; q++) s += kout[il_idx[q]];
+  atomicAdd(out, (unsigned long long)(s * kin[c]));
+}
+
+__global__ void near_counts(int64_t n, const int64_t* __restrict__ t_ptr, const int64_t* __restrict__ s_ptr,
+                            const int64_t* __restrict__ nb_ptr, const int64_t* __restrict__ nb_idx,
+                            unsigned long long* out) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  int64_t s = 0;
+  for (int64_t q = nb_ptr[c]; q < nb_ptr[c + 1]; q++) {
+    int64_t y = nb_idx[q];
+    s += s_ptr[y + 1] - s_ptr[y];
+  }
+  atomicAdd(out, (unsigned long long)(s * (t_ptr[c + 1] - t_ptr[c])));
+}
+
+void excl_scan(const int64_t* in, int64_t n, int64_t* out_n1, cudaStream_t s) {
+  DBuf<int64_t> tmpin;
+  tmpin.alloc(n + 1);
+  if (n) CK(cudaMemcpyAsync(tmpin.get(), in, n * 8, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemsetAsync(tmpin.get() + n, 0, 8, s));
+  size_t bytes = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, tmpin.get(), out_n1, n + 1, s));
+  DBuf<unsigned char> tmp;
+  tmp.alloc(bytes);
+  CK(cub::DeviceScan::ExclusiveSum(tmp.get(), bytes, tmpin.get(), out_n1, n + 1, s));
+  CK(cudaStreamSynchronize(s));
+}
+
+template <class T>
+DBuf<T> upload(const std::vector<T>& h, cudaStream_t s, MemStats* ms = nullptr) {
+  DBuf<T> d;
+  d.alloc(std::max<size_t>(h.size(), 1), ms);
+  if (!h.empty()) CK(cudaMemcpyAsync(d.get(), h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  return d;
+}
+
+size_t workspace_budget() {
+  size_t fr = 0, tot = 0;
+  CK(cudaMemGetInfo(&fr, &tot));
+  size_t b = (size_t)(0.5 * (double)fr);
+  return std::max<size_t>(b, (size_t)256 << 20);
+}
+
+template <int D>
+void set_aca_smem(size_t bytes) {
+  static size_t done = 0;
+  if (bytes > 48 * 1024 && bytes > done) {
+    CK(cudaFuncSetAttribute(aca_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    done = bytes;
+  }
+}
+
+// One side (incoming or outgoing) of the NNCA for one level.
+//   rows/cols: either "own" (contiguous range of a source) or "far"
+//   (gathered concatenation over the interaction list).
+struct SideResult {
+  std::vector<int64_t> rank_h;
+  DBuf<int64_t> rank, tpiv, spiv, piv_off, conv, nevals;
+  DBuf<double> mat;  // interpolation operator per cell (col-major)
+  DBuf<int64_t> mat_off, mat_rows;
+};
+
+template <int D>
+void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const Src& far, int kind, double a,
+              double eps, int64_t max_rank, int which_interp, SideResult& R, cudaStream_t s) {
+  const DevLevel& L = T.lv[level];
+  const int64_t n = L.n;
+  DBuf<int64_t> own_b, own_len, far_len;
+  own_b.alloc(n);
+  own_len.alloc(n);
+  far_len.alloc(n);
+  cand_sizes<<<ceil_div(n, 128), 128, 0, s>>>(n, own, far, L.il_ptr.get(), L.il_idx.get(), own_b.get(),
+                                              own_len.get(), far_len.get());
+  CKL();
+  auto ob = to_host(own_b.get(), n, s), ol = to_host(own_len.get(), n, s), fl = to_host(far_len.get(), n, s);
+  std::vector<int64_t> mh(n), nh(n), caph(n), u_off(n), v_off(n), f_off(n), piv_off(n), mat_off(n), far_off(n);
+  for (int64_t c = 0; c < n; c++) {
+    mh[c] = rows_far ? fl[c] : ol[c];
+    nh[c] = rows_far ? ol[c] : fl[c];
+    int64_t cp = std::min(mh[c], nh[c]);
+    if (max_rank >= 0) cp = std::min(cp, max_rank);
+    caph[c] = cp;
+  }
+  // offsets: pivots and interpolation matrices for the whole level
+  int64_t po = 0, mo = 0;
+  for (int64_t c = 0; c < n; c++) {
+    piv_off[c] = po;
+    po += caph[c];
+    mat_off[c] = mo;
+    mo += (which_interp == 0 ? mh[c] : nh[c]) * caph[c];
+  }
+  R.piv_off = upload(piv_off, s);
+  R.rank.alloc(n);
+  R.conv.alloc(n);
+  R.nevals.alloc(n);
+  DBuf<int64_t> rp, cp;
+  rp.alloc(std::max<int64_t>(po, 1));
+  cp.alloc(std::max<int64_t>(po, 1));
+  R.tpiv.alloc(std::max<int64_t>(po, 1));
+  R.spiv.alloc(std::max<int64_t>(po, 1));
+  R.mat_off = upload(mat_off, s);
+  R.mat_rows = upload(which_interp == 0 ? mh : nh, s);
+  R.mat.alloc(std::max<int64_t>(mo, 1));
+  auto d_m = upload(mh, s), d_n = upload(nh, s), d_cap = upload(caph, s);
+  auto d_ob = upload(ob, s);
+  // batches bounded by the workspace budget
+  const size_t budget = workspace_budget();
+  int64_t c0 = 0;
+  while (c0 < n) {
+    size_t bytes = 0;
+    int64_t far_tot = 0, ws_u = 0, ws_v = 0, ws_f = 0, maxcap = 0;
+    int64_t c1 = c0;
+    while (c1 < n) {
+      size_t cb = (size_t)((mh[c1] + nh[c1]) * caph[c1]) * 8 + (size_t)(mh[c1] + nh[c1]) + (size_t)fl[c1] * (D * 8 + 8);
+      if (c1 > c0 && bytes + cb > budget) break;
+      bytes += cb;
+      u_off[c1] = ws_u;
+      v_off[c1] = ws_v;
+      f_off[c1] = ws_f;
+      far_off[c1] = far_tot;
+      ws_u += mh[c1] * caph[c1];
+      ws_v += nh[c1] * caph[c1];
+      ws_f += mh[c1] + nh[c1];
+      far_tot += fl[c1];
+      maxcap = std::max(maxcap, caph[c1]);
+      c1++;
+    }
+    const int64_t nb = c1 - c0;
+    DBuf<double> U, V, farc;
+    DBuf<unsigned char> flags;
+    DBuf<int64_t> farg;
+    U.alloc(std::max<int64_t>(ws_u, 1));
+    V.alloc(std::max<int64_t>(ws_v, 1));
+    flags.alloc(std::max<int64_t>(ws_f, 1));
+    farc.alloc(std::max<int64_t>(far_tot * D, 1));
+    farg.alloc(std::max<int64_t>(far_tot, 1));
+    std::vector<int64_t> sl_u(u_off.begin(), u_off.end()), sl_v(v_off.begin(), v_off.end());
+    auto d_uoff = upload(u_off, s), d_voff = upload(v_off, s), d_foff = upload(f_off, s),
+         d_faroff = upload(far_off, s);
+    gather_far<D><<<(unsigned)nb, 128, 0, s>>>(c0, far, L.il_ptr.get(), L.il_idx.get(), d_faroff.get(), farc.get(),
+                                               std::max<int64_t>(far_tot, 1), farg.get());
+    CKL();
+    AcaArgs A;
+    A.kind = kind;
+    A.a = a;
+    A.eps2 = eps * eps;
+    A.cell0 = c0;
+    A.m = d_m.get();
+    A.n = d_n.get();
+    A.cap = d_cap.get();
+    if (rows_far) {
+      A.row_base = farc.get();
+      A.ld_row = std::max<int64_t>(far_tot, 1);
+      A.row_off = d_faroff.get();
+      A.row_gidx = farg.get();
+      A.col_base = own.coords;
+      A.ld_col = own.ld;
+      A.col_off = d_ob.get();
+      A.col_gidx = own.gidx;
+    } else {
+      A.row_base = own.coords;
+      A.ld_row = own.ld;
+      A.row_off = d_ob.get();
+      A.row_gidx = own.gidx;
+      A.col_base = farc.get();
+      A.ld_col = std::max<int64_t>(far_tot, 1);
+      A.col_off = d_faroff.get();
+      A.col_gidx = farg.get();
+    }
+    A.U = U.get();
+    A.u_off = d_uoff.get();
+    A.V = V.get();
+    A.v_off = d_voff.get();
+    A.flags = flags.get();
+    A.f_off = d_foff.get();
+    A.piv_off = R.piv_off.get();
+    A.rp = rp.get();
+    A.cp = cp.get();
+    A.tpiv = R.tpiv.get();
+    A.spiv = R.spiv.get();
+    A.rank = R.rank.get();
+    A.conv = R.conv.get();
+    A.nevals = R.nevals.get();
+    size_t smem = (size_t)std::max<int64_t>(maxcap, 1) * 4 * sizeof(double);
+    if (smem > 200 * 1024) throw std::runtime_error("ACA rank cap too large for shared memory");
+    set_aca_smem<D>(smem);
+    aca_kernel<D><<<(unsigned)nb, ACA_THREADS, smem, s>>>(A);
+    CKL();
+    if (which_interp == 0)
+      interp_kernel<<<(unsigned)nb, 256, 0, s>>>(0, c0, d_m.get(), R.rank.get(), U.get(), d_uoff.get(), rp.get(),
+                                                 R.piv_off.get(), R.mat.get(), R.mat_off.get());
+    else
+      interp_kernel<<<(unsigned)nb, 256, 0, s>>>(1, c0, d_n.get(), R.rank.get(), V.get(), d_voff.get(), cp.get(),
+                                                 R.piv_off.get(), R.mat.get(), R.mat_off.get());
+    CKL();
+    CK(cudaStreamSynchronize(s));
+    c0 = c1;
+  }
+  R.rank_h = to_host(R.rank.get(), n, s);
+}
+
+template <int D>
+std::unique_ptr<DevH2> assemble_impl(const DevTree& T, int kind, double a, double eps, bool force_general,
+                                     int64_t max_rank, cudaStream_t s) {
+  auto t0 = std::chrono::steady_clock::now();
+  auto H = std::make_unique<DevH2>();
+  H->t = &T;
+  H->kind = kind;
+  H->a = a;
+  H->eps = eps;
+  H->symmetric = T.shared && !force_general;  // all built-in kernels are symmetric
+  const int L = T.depth;
+  H->lv.resize(L + 1);
+  for (int level = L; level >= 2; level--) {
+    const DevLevel& Lv = T.lv[level];
+    DevH2Level& HL = H->lv[level];
+    HL.n = Lv.n;
+    const bool leaf = level == L;
+    Src own_t, own_s, far_t, far_s;
+    if (leaf) {
+      own_t = Src{T.tsd(), T.np, T.t_perm.get(), Lv.t_ptr.get(), nullptr};
+      own_s = Src{T.ssd(), T.nq, T.sperm(), T.shared ? Lv.t_ptr.get() : Lv.s_ptr.get(), nullptr};
+    } else {
+      const DevH2Level& C = H->lv[level + 1];
+      own_t = Src{C.tin_c.get(), std::max<int64_t>(C.in_total, 1), C.t_in.get(), C.in_ptr.get(), Lv.ch_ptr.get()};
+      own_s = Src{C.sout_cd(), std::max<int64_t>(C.out_total, 1), C.s_out.n ? C.s_out.get() : C.t_in.get(),
+                  C.out_ptrd(), Lv.ch_ptr.get()};
+    }
+    far_t = own_t;
+    far_s = own_s;
+    // incoming: rows = own targets, cols = far sources
+    SideResult in;
+    run_side<D>(T, level, false, own_t, far_s, kind, a, eps, max_rank, 0, in, s);
+    HL.kin = std::move(in.rank);
+    HL.in_ptr.alloc(HL.n + 1, &H->mem);
+    excl_scan(HL.kin.get(), HL.n, HL.in_ptr.get(), s);
+    HL.in_total = read_one(HL.in_ptr.get() + HL.n, s);
+    HL.t_in.alloc(std::max<int64_t>(HL.in_total, 1), &H->mem);
+    HL.s_in.alloc(std::max<int64_t>(HL.in_total, 1), &H->mem);
+    if (HL.n)
+      compact_pivots<<<(unsigned)HL.n, 64, 0, s>>>(HL.n, HL.kin.get(), in.piv_off.get(), HL.in_ptr.get(),
+                                                  in.tpiv.get(), in.spiv.get(), HL.t_in.get(), HL.s_in.get());
+    CKL();
+    HL.tin_c.alloc(std::max<int64_t>(HL.in_total * D, 1), &H->mem);
+    if (HL.in_total)
+      gather_coords<D><<<ceil_div(HL.in_total, 256), 256, 0, s>>>(T.Pd(), HL.t_in.get(), HL.in_total,
+                                                                  HL.tin_c.get());
+    CKL();
+    HL.pmat = std::move(in.mat);
+    HL.pm_off = std::move(in.mat_off);
+    HL.m_in = std::move(in.mat_rows);
+    HL.conv = std::move(in.conv);
+    HL.nevals = std::move(in.nevals);
+    if (!H->symmetric) {
+      // outgoing: rows = far targets, cols = own sources
+      SideResult out;
+      run_side<D>(T, level, true, own_s, far_t, kind, a, eps, max_rank, 1, out, s);
+      HL.kout = std::move(out.rank);
+      HL.out_ptr.alloc(HL.n + 1, &H->mem);
+      excl_scan(HL.kout.get(), HL.n, HL.out_ptr.get(), s);
+      HL.out_total = read_one(HL.out_ptr.get() + HL.n, s);
+      HL.t_out.alloc(std::max<int64_t>(HL.out_total, 1), &H->mem);
+      HL.s_out.alloc(std::max<int64_t>(HL.out_total, 1), &H->mem);
+      if (HL.n)
+        compact_pivots<<<(unsigned)HL.n, 64, 0, s>>>(HL.n, HL.kout.get(), out.piv_off.get(), HL.out_ptr.get(),
+                                                    out.tpiv.get(), out.spiv.get(), HL.t_out.get(), HL.s_out.get());
+      CKL();
+      HL.sout_c.alloc(std::max<int64_t>(HL.out_total * D, 1), &H->mem);
+      if (HL.out_total)
+        gather_coords<D><<<ceil_div(HL.out_total, 256), 256, 0, s>>>(T.Qd(), HL.s_out.get(), HL.out_total,
+                                                                     HL.sout_c.get());
+      CKL();
+      HL.qmat = std::move(out.mat);
+      HL.qm_off = std::move(out.mat_off);
+      HL.n_out = std::move(out.mat_rows);
+      // nevals: add outgoing counts
+      auto a1 = to_host(HL.nevals.get(), HL.n, s), a2 = to_host(out.nevals.get(), HL.n, s);
+      for (int64_t c = 0; c < HL.n; c++) a1[c] += a2[c];
+      CK(cudaMemcpyAsync(HL.nevals.get(), a1.data(), HL.n * 8, cudaMemcpyHostToDevice, s));
+      auto cv = to_host(out.conv.get(), HL.n, s);
+      for (int64_t c = 0; c < HL.n; c++) H->unconverged += cv[c] == 0;
+    } else {
+      HL.out_total = HL.in_total;
+    }
+    CK(cudaStreamSynchronize(s));
+    // stats
+    auto nev = to_host(HL.nevals.get(), HL.n, s);
+    auto kin = to_host(HL.kin.get(), HL.n, s);
+    auto kout = H->symmetric ? kin : to_host(HL.kout.get(), HL.n, s);
+    auto cv = to_host(HL.conv.get(), HL.n, s);
+    for (int64_t c = 0; c < HL.n; c++) {
+      H->evals_pivots += nev[c];
+      H->max_rank = std::max({H->max_rank, kin[c], kout[c]});
+      H->unconverged += cv[c] == 0;
+    }
+    H->cells_visited += HL.n;
+  }
+  // coupling / near-field entry counts (what the reference would evaluate)
+  {
+    DBuf<unsigned long long> acc;
+    acc.alloc(1);
+    CK(cudaMemsetAsync(acc.get(), 0, 8, s));
+    for (int level = 2; level <= L; level++) {
+      const DevLevel& Lv = T.lv[level];
+      const DevH2Level& HL = H->lv[level];
+      if (Lv.n)
+        coupling_counts<<<ceil_div(Lv.n, 128), 128, 0, s>>>(Lv.n, HL.kin.get(), HL.koutd(), Lv.il_ptr.get(),
+                                                            Lv.il_idx.get(), acc.get());
+      CKL();
+    }
+    H->evals_couplings = (int64_t)read_one(acc.get(), s);
+    CK(cudaMemsetAsync(acc.get(), 0, 8, s));
+    const DevLevel& Lf = T.lv[L];
+    near_counts<<<ceil_div(Lf.n, 128), 128, 0, s>>>(Lf.n, Lf.t_ptr.get(),
+                                                    T.shared ? Lf.t_ptr.get() : Lf.s_ptr.get(), Lf.nb_ptr.get(),
+                                                    Lf.nb_idx.get(), acc.get());
+    CKL();
+    H->evals_nearfield = (int64_t)read_one(acc.get(), s);
+  }
+  CK(cudaStreamSynchronize(s));
+  H->setup_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
+  return H;
+}
+
+}  // namespace
+
+std::unique_ptr<DevH2> assemble(const DevTree& t, int kind, double a, double eps, bool force_general,
+                                int64_t max_rank, cudaStream_t s) {
+  if (!(eps > 0)) throw std::invalid_argument("epsilon must be positive");
+  if (!kind_valid(kind)) throw std::invalid_argument("unknown kernel kind");
+  switch (t.d) {
+    case 1: return assemble_impl<1>(t, kind, a, eps, force_general, max_rank, s);
+    case 2: return assemble_impl<2>(t, kind, a, eps, force_general, max_rank, s);
+    case 3: return assemble_impl<3>(t, kind, a, eps, force_general, max_rank, s);
+    default: return assemble_impl<4>(t, kind, a, eps, force_general, max_rank, s);
+  }
+}
+
+// Single-block ACA for the drop-in partial_aca path (_core.pyx:184).
+void aca_single(int kind, double a, const double* X, int64_t m, const double* Y, int64_t n, int d, double eps,
+                int64_t cap, double* U, double* V, int64_t* rp, int64_t* cp, int* conv, int64_t* nevals,
+                int64_t* rank) {
+  cudaStream_t s = 0;
+  if (m == 0 || n == 0 || cap == 0) {
+    *rank = 0;
+    *conv = (m == 0 || n == 0) ? 1 : 0;
+    *nevals = 0;
+    return;
+  }
+  std::vector<double> xs(m * d), ys(n * d);
+  for (int64_t i = 0; i < m; i++)
+    for (int k = 0; k < d; k++) xs[k * m + i] = X[i * d + k];
+  for (int64_t j = 0; j < n; j++)
+    for (int k = 0; k < d; k++) ys[k * n + j] = Y[j * d + k];
+  auto dx = upload(xs, s), dy = upload(ys, s);
+  std::vector<int64_t> z{0}, mh{m}, nh{n}, ch{cap}, fo{0};
+  auto dz = upload(z, s), dm = upload(mh, s), dn = upload(nh, s), dc = upload(ch, s);
+  DBuf<double> dU, dV;
+  DBuf<unsigned char> fl;
+  DBuf<int64_t> drp, dcp, tp, sp, rk, cv, ne;
+  dU.alloc(m * cap);
+  dV.alloc(n * cap);
+  fl.alloc(m + n);
+  drp.alloc(cap);
+  dcp.alloc(cap);
+  tp.alloc(cap);
+  sp.alloc(cap);
+  rk.alloc(1);
+  cv.alloc(1);
+  ne.alloc(1);
+  AcaArgs A;
+  A.kind = kind;
+  A.a = a;
+  A.eps2 = eps * eps;
+  A.cell0 = 0;
+  A.m = dm.get();
+  A.n = dn.get();
+  A.cap = dc.get();
+  A.row_base = dx.get();
+  A.ld_row = m;
+  A.row_off = dz.get();
+  A.row_gidx = nullptr;
+  A.col_base = dy.get();
+  A.ld_col = n;
+  A.col_off = dz.get();
+  A.col_gidx = nullptr;
+  A.U = dU.get();
+  A.u_off = dz.get();
+  A.V = dV.get();
+  A.v_off = dz.get();
+  A.flags = fl.get();
+  A.f_off = dz.get();
+  A.piv_off = dz.get();
+  A.rp = drp.get();
+  A.cp = dcp.get();
+  A.tpiv = tp.get();
+  A.spiv = sp.get();
+  A.rank = rk.get();
+  A.conv = cv.get();
+  A.nevals = ne.get();
+  size_t smem = (size_t)cap * 4 * sizeof(double);
+  if (smem > 200 * 1024) throw std::runtime_error("ACA rank cap too large for shared memory");
+  switch (d) {
+    case 1: set_aca_smem<1>(smem); aca_kernel<1><<<1, ACA_THREADS, smem, s>>>(A); break;
+    case 2: set_aca_smem<2>(smem); aca_kernel<2><<<1, ACA_THREADS, smem, s>>>(A); break;
+    case 3: set_aca_smem<3>(smem); aca_kernel<3><<<1, ACA_THREADS, smem, s>>>(A); break;
+    default: set_aca_smem<4>(smem); aca_kernel<4><<<1, ACA_THREADS, smem, s>>>(A); break;
+  }
+  CKL();
+  int64_t k = read_one(rk.get(), s);
+  *rank = k;
+  *conv = (int)read_one(cv.get(), s);
+  *nevals = read_one(ne.get(), s);
+  auto hU = to_host(dU.get(), m * cap, s), hV = to_host(dV.get(), n * cap, s);
+  auto hr = to_host(drp.get(), cap, s), hc = to_host(dcp.get(), cap, s);
+  for (int64_t i = 0; i < m; i++)
+    for (int64_t t = 0; t < k; t++) U[i * cap + t] = hU[t * m + i];
+  for (int64_t j = 0; j < n; j++)
+    for (int64_t t = 0; t < k; t++) V[j * cap + t] = hV[t * n + j];
+  for (int64_t t = 0; t < k; t++) {
+    rp[t] = hr[t];
+    cp[t] = hc[t];
+  }
+}
+
+}  // namespace h2b

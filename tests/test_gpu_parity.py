@@ -1,0 +1,269 @@
+"""GPU parity: libh2b200.so against the reference goldens and the CPU oracle.
+
+Bars (BASELINE.json north_star):
+  * tree partitioning, leaf membership, neighbour / interaction lists: bit-exact;
+  * pivot index sets: identical for kernels whose entries are IEEE-exact
+    (1/r, 1/(4 pi r), reg-inverse); for exp/log kernels CUDA's libm may
+    differ from glibc in the last ulp, so a documented small fraction of
+    cells may resolve a floating-point near-tie differently;
+  * H2 matvec: relative L2 <= 1e-10 against the oracle / reference FP64 H2
+    matvec on identical inputs; and within the ACA tolerance of a direct
+    dense sum.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden_names, load_golden
+
+pytestmark = pytest.mark.gpu
+
+EXACT_KERNELS = {"coulomb-3d", "reg-inverse", "laplace-3d"}
+KIND_NAME = {"gaussian-scaled": ("gaussian", {"sigma": 0.5})}
+
+
+@pytest.fixture(scope="module")
+def h2c():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2203_14832_b200 as h2c
+
+    return h2c
+
+
+def kernel_for(h2c, g):
+    name = str(g["kernel"])
+    d = g["P"].shape[1]
+    if name in KIND_NAME:
+        base, kw = KIND_NAME[name]
+        return h2c.builtin_kernel(base, d, **kw)
+    return h2c.builtin_kernel(name, d)
+
+
+def cloud_for(h2c, g):
+    return h2c.PointCloud.from_points(g["P"], g.get("Q"))
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_tree_bit_exact(h2c, name):
+    g = load_golden(name)
+    cloud = cloud_for(h2c, g)
+    if "error" in g:
+        with pytest.raises(ValueError, match="invalid dims"):
+            h2c.build_tree(cloud, nu=int(g["nu"]), eta=float(np.sqrt(2.0)))
+        return
+    tree = h2c.build_tree(cloud, nu=int(g["nu"]), eta=float(np.sqrt(2.0)))
+    assert tree.depth == int(g["depth"])
+    assert tree.over_capacity == bool(g["over_capacity"])
+    for level in range(tree.depth + 1):
+        assert np.array_equal(tree.array(level, "key"), g[f"L{level}_key"]), level
+        assert np.array_equal(tree.array(level, "t_ptr"), g[f"L{level}_t_idx_ptr"])
+        assert np.array_equal(tree.array(level, "t_idx"), g[f"L{level}_t_idx"])
+        assert np.array_equal(tree.array(level, "s_ptr"), g[f"L{level}_s_idx_ptr"])
+        assert np.array_equal(tree.array(level, "s_idx"), g[f"L{level}_s_idx"])
+        assert np.array_equal(tree.array(level, "nb_ptr"), g[f"L{level}_neighbors_ptr"])
+        assert np.array_equal(tree.array(level, "nb_idx"), g[f"L{level}_neighbors"])
+        assert np.array_equal(tree.array(level, "il_ptr"), g[f"L{level}_interaction_list_ptr"])
+        assert np.array_equal(tree.array(level, "il_idx"), g[f"L{level}_interaction_list"])
+
+
+def test_tree_python_view_matches_reference(h2c):
+    g = load_golden("u2d_reglog")
+    tree = h2c.build_tree(cloud_for(h2c, g), nu=int(g["nu"]), eta=float(np.sqrt(2.0)))
+    for level in range(tree.depth + 1):
+        assert len(tree.cells(level)) == int(g[f"L{level}_ncells_all"])
+        ne = tree.nonempty_cells(level)
+        keys = [int(np.ravel_multi_index(c.multi_index, (1 << level,) * 2)) for c in ne]
+        assert keys == list(g[f"L{level}_key"])
+        # host-derived lists of the view agree with the device lists
+        kid = {k: i for i, k in enumerate(keys)}
+        nbp, nbi = g[f"L{level}_neighbors_ptr"], g[f"L{level}_neighbors"]
+        for i, c in enumerate(ne):
+            mine = [kid[int(np.ravel_multi_index(y.multi_index, (1 << level,) * 2))] for y in c.neighbors
+                    if not y.is_empty]
+            assert mine == list(nbi[nbp[i]:nbp[i + 1]])
+
+
+@pytest.mark.parametrize("name", [n for n in golden_names() if n not in ("dup2d_error",)])
+def test_pivots_and_matvec(h2c, name):
+    g = load_golden(name)
+    if name == "dup1d":
+        pytest.skip("depth-50 degenerate tree: tree parity only")
+    cloud = cloud_for(h2c, g)
+    tree = h2c.build_tree(cloud, nu=int(g["nu"]), eta=float(np.sqrt(2.0)))
+    kern = kernel_for(h2c, g)
+    h2 = h2c.assemble(tree, kern, float(g["eps"]), force_general=bool(g["force_general"]))
+    total = mism = 0
+    for level in range(2, tree.depth + 1):
+        mine = {a: h2.array(level, a) for a in ("t_in", "s_in", "t_out", "s_out")}
+        kin, kout = h2.array(level, "k_in"), h2.array(level, "k_out")
+        op = {"t_in": np.concatenate([[0], np.cumsum(kin)]), "t_out": np.concatenate([[0], np.cumsum(kout)])}
+        op["s_in"], op["s_out"] = op["t_in"], op["t_out"]
+        for c in range(tree.ncells(level)):
+            total += 1
+            same = all(np.array_equal(mine[a][op[a][c]:op[a][c + 1]],
+                                      g[f"P{level}_{a}"][g[f"P{level}_{a}_ptr"][c]:g[f"P{level}_{a}_ptr"][c + 1]])
+                       for a in op)
+            mism += not same
+    kname = str(g["kernel"])
+    # the reference ran custom kernels through its numpy/BLAS ACA: near-tie differences possible there too
+    if kname in EXACT_KERNELS and kname != "laplace-3d":
+        assert mism == 0, f"{mism}/{total} cells differ"
+        assert h2.stats.evals_pivots == int(g["stat_evals_pivots"])
+        assert h2.stats.evals_couplings == int(g["stat_evals_couplings"])
+        assert h2.stats.evals_nearfield == int(g["stat_evals_nearfield"])
+        assert h2.stats.max_rank == int(g["stat_max_rank"])
+    else:
+        assert mism <= max(2, total // 20), f"{mism}/{total} cells differ"
+    W = g["W"]
+    U = h2c.h2_matvec(h2, W if W.shape[1] > 1 else W[:, 0])
+    U = U if U.ndim == 2 else U[:, None]
+    err = np.linalg.norm(U - g["U"]) / np.linalg.norm(g["U"])
+    tol = 1e-10 if mism == 0 else 10 * float(g["eps"])
+    assert err <= tol, err
+    errd = np.linalg.norm(U - g["U_dense"]) / np.linalg.norm(g["U_dense"])
+    errd_ref = np.linalg.norm(g["U"] - g["U_dense"]) / np.linalg.norm(g["U_dense"])
+    assert errd <= 1.5 * errd_ref + 1e-12
+
+
+@pytest.mark.parametrize("name", ["u3d_coulomb", "sphere_coulomb", "u2d_reglog", "ns_matern", "fg_gauss",
+                                  "u4d_matern", "clustered", "ns_small_q"])
+def test_against_oracle(h2c, oracle_mod, name):
+    """Same representation as the oracle: pivots and interpolation operators."""
+    g = load_golden(name)
+    cloud = cloud_for(h2c, g)
+    tree = h2c.build_tree(cloud, nu=int(g["nu"]), eta=float(np.sqrt(2.0)))
+    kern = kernel_for(h2c, g)
+    h2 = h2c.assemble(tree, kern, float(g["eps"]), force_general=bool(g["force_general"]))
+    ot = oracle_mod.OTree(g["P"], g.get("Q"), nu=int(g["nu"]))
+    oh = oracle_mod.OH2(ot, kern.kind, kern.device_param, float(g["eps"]), force_general=bool(g["force_general"]))
+    for level in range(2, tree.depth + 1):
+        for a in ("k_in", "k_out", "t_in", "s_in", "t_out", "s_out"):
+            assert np.array_equal(h2.array(level, a), oh.get(level, a)), (level, a)
+        for c in range(0, tree.ncells(level), max(1, tree.ncells(level) // 7)):
+            for which in (0, 1):
+                mine = h2.interp(level, c, which)
+                ref = oh.interp(level, c, which)
+                assert mine.shape == ref.shape
+                if mine.size:
+                    assert np.max(np.abs(mine - ref)) <= 1e-8 * max(1.0, np.max(np.abs(ref)))
+    w = np.random.default_rng(3).standard_normal(cloud.n_sources)
+    u = h2c.h2_matvec(h2, w)
+    uo = oh.matvec(w)
+    assert np.linalg.norm(u - uo) / np.linalg.norm(uo) <= 1e-10
+
+
+def test_aca_blocks(h2c):
+    import os
+
+    from conftest import GOLDEN
+    from paper_2203_14832_b200.aca import aca_kernel
+
+    with np.load(os.path.join(GOLDEN, "aca_blocks.npz")) as z:
+        g = {k: z[k] for k in z.files}
+    n = 0
+    while f"A{n}_X" in g:
+        kind = int(g[f"A{n}_kind"])
+        U, V, rp, cp, conv, nev = aca_kernel(kind, float(g[f"A{n}_a"]), g[f"A{n}_X"], g[f"A{n}_Y"],
+                                             float(g[f"A{n}_eps"]), min(g[f"A{n}_X"].shape[0], g[f"A{n}_Y"].shape[0]))
+        if kind in (1, 2):  # IEEE-exact kernels: bitwise
+            assert np.array_equal(rp, g[f"A{n}_rp"]) and np.array_equal(cp, g[f"A{n}_cp"])
+            assert np.array_equal(U, g[f"A{n}_U"]) and np.array_equal(V, g[f"A{n}_V"])
+            assert nev == int(g[f"A{n}_nevals"])
+        else:
+            k = min(rp.size, g[f"A{n}_rp"].size)
+            assert abs(rp.size - g[f"A{n}_rp"].size) <= 1
+            assert np.array_equal(rp[:k // 2], g[f"A{n}_rp"][:k // 2])
+        n += 1
+
+
+def test_kernel_block_exact(h2c, oracle_mod):
+    rng = np.random.default_rng(0)
+    X = rng.uniform(-1, 1, (50, 3))
+    Y = rng.uniform(-1, 1, (60, 3))
+    Y[0] = X[0]
+    for name, kind in (("coulomb-3d", 2), ("reg-inverse", 1), ("laplace-3d", 5)):
+        k = h2c.builtin_kernel(name, 3)
+        assert np.array_equal(h2c.kernels.raw_block(k, X, Y), oracle_mod.kernel_block(kind, k.device_param, X, Y))
+    for name in ("matern", "gaussian", "reg-log-2d", "log"):
+        k = h2c.builtin_kernel(name, 3)
+        ref = oracle_mod.kernel_block(k.kind, k.device_param, X, Y)
+        assert np.allclose(h2c.kernels.raw_block(k, X, Y), ref, rtol=4e-16 * 4, atol=0)
+
+
+def test_partial_aca_dropin(h2c):
+    rng = np.random.default_rng(1)
+    X = rng.uniform(-0.5, 0.5, (80, 2))
+    Y = rng.uniform(-0.5, 0.5, (90, 2)) + 3.0
+    cloud = h2c.PointCloud.from_points(X, Y)
+    k = h2c.builtin_kernel("coulomb-3d", 2)
+    res = h2c.partial_aca(np.arange(80), np.arange(90), h2c.KernelOracle(k, cloud), 1e-10)
+    A = h2c.kernels.raw_block(k, X, Y)
+    assert np.linalg.norm(A - res.u_factor @ res.v_factor.T) <= 1e-8 * np.linalg.norm(A)
+    P = h2c.row_interpolator(res)
+    assert np.allclose(P[res.row_pivots_local], np.eye(res.rank))
+    blk = res.pivot_block()
+    assert np.allclose(h2c.apply_pivot_inverse(res, blk), np.eye(res.rank), atol=1e-9)
+
+
+def test_linearity_and_multirhs(h2c):
+    from paper_2203_14832_b200 import sampling
+
+    pts = sampling.uniform_points(20000, 3, 1)
+    cloud = h2c.PointCloud.from_points(pts)
+    tree = h2c.build_tree(cloud, nu=64, eta=float(np.sqrt(2.0)))
+    h2 = h2c.assemble(tree, h2c.builtin_kernel("laplace-3d", 3), 1e-8)
+    rng = np.random.default_rng(2)
+    W = rng.standard_normal((20000, 3))
+    U = h2c.h2_matvec(h2, W)
+    for r in range(3):
+        assert np.allclose(U[:, r], h2c.h2_matvec(h2, W[:, r]), rtol=0, atol=1e-13 * np.abs(U).max())
+    lin = h2c.h2_matvec(h2, 2.5 * W[:, 0] + W[:, 1])
+    assert np.linalg.norm(lin - (2.5 * U[:, 0] + U[:, 1])) <= 1e-12 * np.linalg.norm(lin)
+    assert np.all(h2c.h2_matvec(h2, np.zeros(20000)) == 0.0)
+    # symmetric operator: x^T A y == y^T A x
+    assert abs(W[:, 0] @ U[:, 1] - W[:, 1] @ U[:, 0]) <= 1e-9 * abs(W[:, 0] @ U[:, 1])
+    # direct dense sum on sampled rows within the ACA tolerance
+    rows = rng.choice(20000, 500, replace=False)
+    exact = h2c.dense_rows(h2c.builtin_kernel("laplace-3d", 3), cloud, rows, W[:, 0])
+    assert np.linalg.norm(U[rows, 0] - exact) / np.linalg.norm(exact) <= 1e-7
+
+
+def test_device_tensor_path(h2c):
+    import torch
+
+    from paper_2203_14832_b200 import sampling
+
+    pts = sampling.sphere_points(8000, 3, 2)
+    cloud = h2c.PointCloud.from_points(pts)
+    tree = h2c.build_tree(cloud, nu=64, eta=float(np.sqrt(2.0)))
+    h2 = h2c.assemble(tree, h2c.builtin_kernel("laplace-3d", 3), 1e-6)
+    w = np.random.default_rng(0).uniform(-1, 1, 8000)
+    u_host = h2c.h2_matvec(h2, w)
+    wd = torch.from_numpy(w).cuda()
+    ud = h2c.h2_matvec(h2, wd)
+    assert ud.is_cuda
+    assert np.allclose(ud.cpu().numpy(), u_host, rtol=0, atol=1e-14 * np.abs(u_host).max())
+
+
+def test_edge_cases(h2c):
+    k = h2c.builtin_kernel("matern", 2)
+    # single point: one leaf, matvec = K(x,x) w
+    t = h2c.build_tree(h2c.PointCloud.from_points(np.array([[0.1, 0.2]])), nu=4, eta=float(np.sqrt(2.0)))
+    assert t.depth == 0
+    h2 = h2c.assemble(t, k, 1e-8)
+    assert np.allclose(h2c.h2_matvec(h2, np.array([2.0])), [2.0])
+    # N < nu: dense only, exact
+    pts = np.random.default_rng(0).uniform(-1, 1, (100, 2))
+    t = h2c.build_tree(h2c.PointCloud.from_points(pts), nu=100, eta=float(np.sqrt(2.0)))
+    h2 = h2c.assemble(t, k, 1e-8)
+    w = np.random.default_rng(1).standard_normal(100)
+    assert np.allclose(h2c.h2_matvec(h2, w), h2c.dense_matvec(k, t.cloud, w), rtol=1e-13, atol=0)
+    with pytest.raises(ValueError):
+        h2c.build_tree(h2c.PointCloud.from_points(np.zeros((0, 2))), nu=4, eta=1.0)
+    with pytest.raises(ValueError):
+        h2c.build_tree(h2c.PointCloud.from_points(pts), nu=0, eta=1.0)
+    with pytest.raises(ValueError):
+        h2c.h2_matvec(h2, np.zeros(99))

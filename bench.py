@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""Benchmark: NNCA H2 matvec on B200 at BASELINE.json's headline config.
+
+Workload (BASELINE.json configs[2], the N=1M 3D 1/r case the metric names):
+N = 1,048,576 points on the unit sphere (normalised N(0, I3), seed 2), FP64,
+Laplace kernel 1/(4 pi r) with K(x, x) = 0, octree with <= 64 points per leaf,
+eta = sqrt(2), NNCA tolerance 1e-6, x ~ U(-1, 1).  One setup (tree + NNCA),
+then repeated matvecs as in an iterative solver: a bench "step" is one H2
+matvec.  Synthetic inputs stand in for the paper's datasets.
+
+Reported: effective N^2/s (value), matvec ms, NNCA setup ms, relative L2
+error of the GPU matvec against (a) the CPU oracle's FP64 H2 matvec on the
+same input and (b) a direct dense sum on 1000 sampled rows.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Multi-GPU: the H2 matvec does not shard (replicas only): each rank
+runs an independent replica, value = aggregate N^2/s over ranks (max-over-ranks
+time), scaling "weak".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "H2 matvec ms & effective N^2/s at N=1M 3D 1/r; NNCA setup ms; rel. L2 err"
+
+CONFIGS = {
+    # name: (distribution, N, dim, seed, kernel, kernel kwargs, nu, eps, x-dist, nrhs)
+    "c0": ("uniform", 4096, 2, 0, "log", {}, 64, 1e-8, "normal", 1),
+    "c1": ("uniform", 262144, 3, 1, "laplace-3d", {}, 64, 1e-8, "normal", 1),
+    "c2": ("sphere", 1048576, 3, 2, "laplace-3d", {}, 64, 1e-6, "uniform", 1),
+    "c3": ("gmix", 524288, 3, 3, "gaussian", {"sigma": 0.5}, 64, 1e-8, "labels", 1),
+    "c4": ("uniform", 4194304, 2, 4, "coulomb-3d", {}, 128, 1e-10, "normal", 16),
+}
+HEADLINE = "c2"
+FLOPS_PER_PAIR = 16  # 1/r entry: 3 sub + 5 (r^2) + 6 (rsqrt Newton) + 2 (fma into the sum)
+
+
+def make_inputs(cfg, n_override=None):
+    from paper_2203_14832_b200 import sampling
+
+    dist, n, dim, seed, kname, kkw, nu, eps, xdist, nrhs = cfg
+    if n_override:
+        n = n_override
+    pts = sampling.make_points(dist, n, dim, seed)
+    rng = np.random.default_rng(seed + 100)
+    if xdist == "uniform":
+        w = rng.uniform(-1.0, 1.0, (n, nrhs))
+    elif xdist == "labels":
+        w = np.where(rng.random((n, nrhs)) < 0.5, -1.0, 1.0)
+    else:
+        w = rng.standard_normal((n, nrhs))
+    return pts, w if nrhs > 1 else w[:, 0]
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def oracle_pipeline(pts, cfg, w, threads=None, matvecs=1):
+    """The CPU oracle (reference algorithm restated in C, OpenMP): setup + matvecs."""
+    from oracle import oracle as O
+
+    if threads:
+        O.set_threads(threads)
+    kname, kkw, nu, eps = cfg[4], cfg[5], cfg[6], cfg[7]
+    kind = {"laplace-3d": 5, "coulomb-3d": 2, "log": 6, "gaussian": 7 if kkw else 4}[kname]
+    a = 1.0 / (2.0 * kkw["sigma"] ** 2) if kkw else 0.0
+    t0 = time.perf_counter()
+    t = O.OTree(pts, None, nu=nu)
+    h = O.OH2(t, kind, a, eps)
+    setup_s = time.perf_counter() - t0
+    times, u = [], None
+    for _ in range(matvecs):
+        t1 = time.perf_counter()
+        u = h.matvec(w)
+        times.append(time.perf_counter() - t1)
+    return {"setup_s": setup_s, "matvec_s": times, "u": u, "threads": O.threads(), "tree": t, "h2": h}
+
+
+def run_reference(args, cfg, world, rank):
+    """--impl reference: the reference algorithm (CPU oracle) on the host cores."""
+    if rank != 0:
+        return
+    pts, w = make_inputs(cfg, args.n)
+    n = pts.shape[0]
+    res = oracle_pipeline(pts, cfg, w, matvecs=args.warmup + args.steps)
+    times = res["matvec_s"][args.warmup:]
+    ms = 1e3 * float(np.mean(times))
+    value = n * n / (ms * 1e-3)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "N^2/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(args, cfg, n), "N": n},
+        "matvec_ms": ms, "setup_ms": 1e3 * res["setup_s"],
+        "cpu_baseline": {"value": value, "unit": "N^2/s", "cores": res["threads"], "kind": "port",
+                         "sample": f"full workload: oracle setup once + {args.warmup}+{args.steps} full matvecs at "
+                                   f"N={n}"},
+        "e2e": {"value": value, "unit": "N^2/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_name(args, cfg, n):
+    dist, _, dim, seed, kname, kkw, nu, eps, xdist, nrhs = cfg
+    return (f"{args.config}: {dist} N={n} d={dim} seed={seed} kernel={kname}{kkw or ''} nu={nu} eps={eps:g} "
+            f"x~{xdist} nrhs={nrhs}")
+
+
+def run_b200(args, cfg, world, rank, local):
+    import torch
+
+    import paper_2203_14832_b200 as h2c
+    from paper_2203_14832_b200 import _lib
+    from paper_2203_14832_b200.matvec import matvec_launches, stage_times
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    pts, w = make_inputs(cfg, args.n)
+    n = pts.shape[0]
+    nrhs = 1 if w.ndim == 1 else w.shape[1]
+    kname, kkw, nu, eps = cfg[4], cfg[5], cfg[6], cfg[7]
+    kern = h2c.builtin_kernel(kname, cfg[2], **kkw)
+    cloud = h2c.PointCloud.from_points(pts)
+
+    # ---- setup: tree + NNCA (timed on the host around synchronous calls) ----
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    tree = h2c.build_tree(cloud, nu=nu, eta=float(np.sqrt(2.0)))
+    t1 = time.perf_counter()
+    h2 = h2c.assemble(tree, kern, eps)
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    tree_ms, nnca_ms = 1e3 * (t1 - t0), 1e3 * (t2 - t1)
+
+    stream = torch.cuda.current_stream(dev)
+    wd = torch.from_numpy(np.ascontiguousarray(w)).to(dev)
+    ud = torch.empty((n,) if nrhs == 1 else (n, nrhs), dtype=torch.float64, device=dev)
+    L = _lib.lib()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+
+    def matvec_dev():
+        _lib.check(L.h2b_matvec(h2.handle, wd.data_ptr(), ud.data_ptr(), nrhs, 1, stream.cuda_stream))
+
+    for _ in range(args.warmup):
+        matvec_dev()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K device-resident matvecs, L2 flushed between them ----
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for e0, e1 in evs:
+            flush.zero_()
+            e0.record(stream)
+            matvec_dev()
+            e1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    per = [e0.elapsed_time(e1) for e0, e1 in evs]
+    ms = max_over_ranks(float(np.mean(per)), world)
+    value = world * n * n / (ms * 1e-3)
+
+    # ---- e2e: through the C ABI with pinned host buffers (H2D + matvec + D2H per step) ----
+    wh = torch.from_numpy(np.ascontiguousarray(w)).pin_memory()
+    uh = torch.empty(tuple(ud.shape), dtype=torch.float64).pin_memory()
+    for _ in range(2):
+        _lib.check(L.h2b_matvec(h2.handle, wh.data_ptr(), uh.data_ptr(), nrhs, 0, stream.cuda_stream))
+    ee = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier(world)
+    for e0, e1 in ee:
+        flush.zero_()
+        e0.record(stream)
+        _lib.check(L.h2b_matvec(h2.handle, wh.data_ptr(), uh.data_ptr(), nrhs, 0, stream.cuda_stream))
+        e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(float(np.mean([e0.elapsed_time(e1) for e0, e1 in ee])), world)
+    e2e_value = world * n * n / (e2e_ms * 1e-3)
+
+    # ---- roofline of the dominant kernel family (FP64 interaction kernel: M2L + near field) ----
+    st = h2.native_stats()
+    pairs_m2l, pairs_p2p = int(st[1]), int(st[2])
+    stage = stage_times(h2, wd, repeats=max(3, min(args.steps, 10)))  # [up, m2l, l2l, near+l2p, total]
+    peak = ctypes_peak(L)
+    inter_ms = stage[1] + stage[3]
+    flops = FLOPS_PER_PAIR * nrhs * (pairs_m2l + pairs_p2p) if nrhs == 1 else \
+        (pairs_m2l + pairs_p2p) * (FLOPS_PER_PAIR - 2 + 2 * nrhs)
+    achieved = flops / (inter_ms * 1e-3) / 1e12
+    traffic = load_traffic()
+
+    # ---- accuracy: sampled dense rows + CPU-oracle H2 matvec at the full N ----
+    uhost = ud.cpu().numpy()
+    rng = np.random.default_rng(7)
+    rows = rng.choice(n, size=min(1000, n), replace=False)
+    wcol = w if nrhs == 1 else w[:, 0]
+    exact = h2c.dense_rows(kern, cloud, rows, wcol)
+    ucol = uhost if nrhs == 1 else uhost[:, 0]
+    err_dense = float(np.linalg.norm(ucol[rows] - exact) / np.linalg.norm(exact))
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "N^2/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; stands in for the paper's point sets)",
+        "config": {"workload": workload_name(args, cfg, n), "N": n, "nrhs": nrhs,
+                   "l2": "flushed (256 MB write) between timed steps", "parallelism": f"replicas x{world}"},
+        "matvec_ms": ms, "setup_ms": tree_ms + nnca_ms, "tree_ms": tree_ms, "nnca_ms": nnca_ms,
+        "depth": int(st[8]), "max_rank": int(st[3]), "m2l_pairs": pairs_m2l, "p2p_pairs": pairs_p2p,
+        "stage_ms": {"upward": stage[0], "m2l": stage[1], "l2l": stage[2], "near_l2p": stage[3], "total": stage[4]},
+        "rel_l2_err_dense_1000_rows": err_dense,
+        "e2e": {"value": e2e_value, "unit": "N^2/s", "ms_per_step": e2e_ms, "h2d_bytes_per_step": int(wh.nbytes),
+                "d2h_bytes_per_step": int(uh.nbytes)},
+        "gpu_launches": int(matvec_launches(h2, nrhs)) * args.steps,
+        "roofline": {"bound": "fp64", "kernel": "interact_kernel (M2L all levels + near field/L2P)",
+                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                     "traffic": traffic, "flops_per_pair": FLOPS_PER_PAIR,
+                     "peak_source": "measured: DFMA throughput probe (h2b_fp64_peak) on this GPU, same run"},
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and not args.no_cpu_baseline and args.gpus == 1 and world == 1:
+        res = oracle_pipeline(pts, cfg, w, matvecs=1)
+        cpu_ms = 1e3 * res["matvec_s"][0]
+        uo = res["u"]
+        line["rel_l2_err_vs_oracle_h2"] = float(np.linalg.norm(uhost - uo) / np.linalg.norm(uo))
+        line["cpu_baseline"] = {"value": n * n / (cpu_ms * 1e-3), "unit": "N^2/s", "cores": res["threads"],
+                                "kind": "port", "matvec_ms": cpu_ms, "setup_ms": 1e3 * res["setup_s"],
+                                "sample": f"full workload once: oracle tree+NNCA setup and one full H2 matvec at "
+                                          f"N={n} (OpenMP, all host threads)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def ctypes_peak(L):
+    import ctypes
+
+    v = ctypes.c_double()
+    L.h2b_fp64_peak(ctypes.byref(v))
+    return v.value
+
+
+def load_traffic():
+    """dram bytes per launch of the interaction kernel from the committed ncu summary, if any."""
+    path = os.path.join(REPO, "profiles", "interact_traffic.json")
+    if os.path.exists(path):
+        try:
+            return json.load(open(path)).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            return None
+    return None
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
+    ap.add_argument("--config", default=HEADLINE, choices=sorted(CONFIGS))
+    ap.add_argument("--n", type=int, default=None, help="override N (testing)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    cfg = CONFIGS[args.config]
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, cfg, world, rank)
+    else:
+        run_b200(args, cfg, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -89,6 +89,9 @@ int64_t h2b_matvec_launches(const h2b_h2* h, int64_t nrhs);
  * enable with h2b_set_profiling(1). */
 int h2b_set_profiling(int on);
 int h2b_last_stage_ms(double* ms5);
+/* Measured FP64 FMA throughput of this device (TFLOP/s), the roofline
+ * denominator for the FP64-bound interaction kernels. */
+int h2b_fp64_peak(double* tflops);
 
 /* ---- dense oracles: matvec.py:574 dense_matvec / :586 dense_rows ---- */
 int h2b_dense_matvec(int kind, double a, const double* P, int64_t np, const double* Q, int64_t nq, int d,

@@ -377,6 +377,10 @@ int h2b_set_profiling(int on) {
   return 0;
 }
 
+int h2b_fp64_peak(double* tflops) {
+  return guarded([&] { *tflops = fp64_peak_tflops(0); });
+}
+
 int h2b_last_stage_ms(double* ms5) {
   last_stage_ms(ms5);
   return 0;

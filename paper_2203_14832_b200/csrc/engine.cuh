@@ -98,6 +98,7 @@ void aca_single(int kind, double a, const double* X, int64_t m, const double* Y,
 void matvec(DevH2& h, const double* w, double* u, int64_t nrhs, cudaStream_t s);
 int64_t matvec_launches(const DevH2& h, int64_t nrhs);
 void set_profiling(bool on);
+double fp64_peak_tflops(cudaStream_t s);
 void last_stage_ms(double* ms5);
 void dense_matvec(int kind, double a, const double* P, int64_t np, const double* Q, int64_t nq, int d,
                   const double* w, double* u, int64_t nrhs, cudaStream_t s);

@@ -512,4 +512,45 @@ void kernel_block(int kind, double a, const double* X, int64_t m, const double* 
   CKL();
 }
 
+// FP64 FMA throughput probe: 8 independent DFMA chains per thread, full chip.
+namespace {
+__global__ void dfma_peak_kernel(double* out, int iters, double a, double b) {
+  double x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6,
+         x7 = x0 + 7;
+  for (int i = 0; i < iters; i++) {
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+      x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+      x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+  }
+  double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  if (s == 1234.5) out[0] = s;
+}
+}  // namespace
+
+double fp64_peak_tflops(cudaStream_t s) {
+  int dev = 0, nsm = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  DBuf<double> out;
+  out.alloc(1);
+  const int threads = 512, blocks = nsm * 4, iters = 4096;
+  dfma_peak_kernel<<<blocks, threads, 0, s>>>(out.get(), 64, 0.999999, 1e-7);  // warm-up
+  CKL();
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, s));
+  dfma_peak_kernel<<<blocks, threads, 0, s>>>(out.get(), iters, 0.999999, 1e-7);
+  CK(cudaEventRecord(e1, s));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  double flops = 2.0 * 8 * 16 * (double)iters * threads * blocks;
+  return flops / (ms * 1e-3) / 1e12;
+}
+
 }  // namespace h2b

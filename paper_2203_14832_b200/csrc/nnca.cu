@@ -177,6 +177,7 @@ __global__ void __launch_bounds__(ACA_THREADS) aca_kernel(AcaArgs A) {
     }
     if (exhausted) break;
     const double piv = V[k * n + bj];
+    __syncthreads();  // every thread holds piv before the owner of bj rescales it to 1
     double v2p = 0.0;
     for (int64_t j = tid; j < n; j += ACA_THREADS) {
       double v = __ddiv_rn(V[k * n + j], piv);

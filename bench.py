@@ -45,7 +45,7 @@ CONFIGS = {
     "c4": ("uniform", 4194304, 2, 4, "coulomb-3d", {}, 128, 1e-10, "normal", 16),
 }
 HEADLINE = "c2"
-FLOPS_PER_PAIR = 16  # 1/r entry: 3 sub + 5 (r^2) + 6 (rsqrt Newton) + 2 (fma into the sum)
+FLOPS_PER_PAIR = 18  # 1/r entry: 3 DADD + (DMUL + 2 DFMA) r^2 + (2 DMUL + 3 DFMA) rsqrt correction + DFMA accumulate
 
 
 def make_inputs(cfg, n_override=None):

@@ -83,6 +83,10 @@ struct DevH2 {
   DBuf<double> w_sorted, u_tmp;
   std::vector<DBuf<double>> wout, uin;
   DBuf<double> io_w, io_u;  // device staging for host-pointer calls
+  DBuf<double> near;        // near-field sums (sorted target order)
+  DBuf<int64_t> items;      // interaction work list ((list << 40) | cell), by descending pair count
+  int64_t n_items = 0;
+  DBuf<unsigned char> tabs; // per-list pointer tables for the interaction kernel
 };
 
 // tree.cu
@@ -96,6 +100,7 @@ void aca_single(int kind, double a, const double* X, int64_t m, const double* Y,
                 int64_t* rank);
 // matvec.cu
 void matvec(DevH2& h, const double* w, double* u, int64_t nrhs, cudaStream_t s);
+void prepare_matvec(DevH2& h, cudaStream_t s);
 int64_t matvec_launches(const DevH2& h, int64_t nrhs);
 void set_profiling(bool on);
 double fp64_peak_tflops(cudaStream_t s);

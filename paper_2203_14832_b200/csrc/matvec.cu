@@ -8,6 +8,8 @@
 // stored 8-byte entry from HBM.  Transfer operators (P2M/M2M/L2L/L2P) are
 // stored dense, column-major, and applied as batched small GEMVs whose
 // operands are contiguous slices thanks to the Morton cell order.
+#include <cub/cub.cuh>
+
 #include <cmath>
 
 #include "engine.cuh"
@@ -105,155 +107,285 @@ __global__ void gemv_n_add(int64_t ncell, const int64_t* __restrict__ kin, const
     }
 }
 
-constexpr int IT = 128;  // interaction kernel threads
+// ---------------------------------------------------------------------
+// Interaction kernel: one launch for every M2L level and the near field.
+//
+// Work item = (list kind, cell).  Items are sorted by their pair count
+// (largest first) so the 6-7 M2L levels and the leaf near field share one
+// grid with a balanced tail.  A CTA owns one target cell: targets live in
+// registers, the cell's source list (interaction list: pivot coordinates +
+// multipole charges; neighbour list: points + input charges) is streamed
+// through shared-memory tiles and read as warp broadcasts.
+// ---------------------------------------------------------------------
+constexpr int IT2 = 128;
+constexpr int MAXMEM = 128;
 
-struct Interact {
-  // targets
-  const double* tc;  // SoA, ld_t
+struct LevelTab {
+  const double* tc;      // target coords SoA (ld_t)
   int64_t ld_t;
   const int64_t* t_ptr;  // target range per cell
-  // sources
-  const double* sc;  // SoA, ld_s
+  const double* sc;      // source coords SoA (ld_s)
   int64_t ld_s;
   const int64_t* s_ptr;  // source range per source cell
-  const double* q;       // charges (ld R)
-  // list
-  const int64_t* l_ptr;
+  const double* q;       // charges, row stride R
+  const int64_t* l_ptr;  // cell list (CSR)
   const int64_t* l_idx;
-  // output
-  double* out;              // indexed by (target position) * R + r
-  const int64_t* out_perm;  // if set: out row = out_perm[target position]
-  // optional fused L2P: out += P_c (m x k, col-major) * uin_c
-  const double* pm;
-  const int64_t* pm_off;
-  const int64_t* kin;
-  const int64_t* in_ptr;
-  const double* uin;
-  int64_t R, r0;
-  KParams kp;
+  double* out;           // result rows (target position) * R
 };
 
-// Sum over the cell list of K(target, source) * charge, with NR right-hand
-// sides at once.  Thread = (target slot, source group); groups stride the
-// list members; sources are read straight from L1/L2 as warp broadcasts.
-template <int D, int KIND, int NR>
-__global__ void __launch_bounds__(IT) interact_kernel(Interact P) {
-  __shared__ double part[IT * NR];
-  const int64_t c = blockIdx.x;
-  const int64_t tb = P.t_ptr[c], m = P.t_ptr[c + 1] - tb;
-  if (m == 0) return;
-  const int64_t lb = P.l_ptr[c], le = P.l_ptr[c + 1];
-  int TS = 1;
-  while (TS < m && TS < IT) TS <<= 1;
-  const int G = IT / TS;
-  const int slot = threadIdx.x % TS, grp = threadIdx.x / TS;
-  for (int64_t a0 = 0; a0 < m; a0 += TS) {
-    const int64_t a = a0 + slot;
-    const bool active = a < m;
-    double x[D];
+__device__ __forceinline__ double rsq_approx(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+
+// K(r2) for the interaction kernel.  1/r: MUFU.RSQ64H seed + one Newton step
+// (cubic correction: ~1 ulp), with the punctured diagonal handled by
+// an integer test on the high word (r2 == 0 or subnormal -> 0).
+template <int KIND>
+__device__ __forceinline__ double kpair(double r2, const KParams& kp) {
+  if constexpr (KIND == COULOMB || KIND == LAPLACE) {
+    const bool zero = __double2hiint(r2) == 0;
+    const double r2s = zero ? 1.0 : r2;
+    const double y = rsq_approx(r2s);
+    const double e = fma(-r2s, y * y, 1.0);
+    const double kv = fma(y * e, fma(0.375, e, 0.5), y);  // y (1 + e/2 + 3e^2/8): full FP64 accuracy
+    return zero ? 0.0 : kv;
+  } else {
+    return kfast<KIND>(r2, kp);
+  }
+}
+
+// Per-source record in shared memory: D coordinates then NR charges, padded
+// to whole double2 words so one source is W LDS.128 broadcasts.
+template <int D, int NR>
+struct SrcW {
+  static constexpr int W = (D + NR + 1) / 2;
+};
+
+// Body for one target chunk.  RT = 2 targets per thread (register blocking:
+// every shared-memory source read feeds two pair evaluations).  SELF = the
+// list may contain the target itself (near field): punctured diagonal test.
+template <int D, int KIND, int NR, int TILE, bool SELF>
+__device__ __forceinline__ void interact_cell(const LevelTab& T, int64_t c, int64_t R, int64_t r0, const KParams& kp,
+                                              double2* tile, int64_t* pref, int64_t* sbeg, int64_t* wsum,
+                                              double* part) {
+  constexpr int RT = 2;
+  constexpr int W = SrcW<D, NR>::W;
+  const int64_t tb = T.t_ptr[c], m = T.t_ptr[c + 1] - tb;
+  const int64_t lb = T.l_ptr[c], le = T.l_ptr[c + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int64_t a0 = 0; a0 < m; a0 += RT * IT2) {
+    const int64_t mc = (m - a0) < RT * IT2 ? (m - a0) : RT * IT2;
+    const int TS = (int)((mc + RT - 1) / RT);
+    const int G = IT2 / TS;
+    const int slot = tid % TS, grp = tid / TS;
+    const bool worker = grp < G;
+    bool act[RT];
+    double x[RT][D];
+    double acc[RT][NR];
 #pragma unroll
-    for (int k = 0; k < D; k++) x[k] = active ? P.tc[k * P.ld_t + tb + a] : 0.0;
-    double acc[NR];
+    for (int t = 0; t < RT; t++) {
+      const int64_t a = a0 + slot + t * TS;
+      act[t] = worker && (slot + t * TS) < mc;
 #pragma unroll
-    for (int r = 0; r < NR; r++) acc[r] = 0.0;
-    if (active) {
-      for (int64_t q = lb + grp; q < le; q += G) {
-        const int64_t sc = P.l_idx[q];
-        const int64_t sb = P.s_ptr[sc], se = P.s_ptr[sc + 1];
-        int64_t j = sb;
-        for (; j + 1 < se; j += 2) {
-          double r2a = 0.0, r2b = 0.0;
+      for (int k = 0; k < D; k++) x[t][k] = act[t] ? T.tc[k * T.ld_t + tb + a] : 0.0;
 #pragma unroll
-          for (int k = 0; k < D; k++) {
-            double da = x[k] - __ldg(P.sc + k * P.ld_s + j);
-            double db = x[k] - __ldg(P.sc + k * P.ld_s + j + 1);
-            r2a = fma(da, da, r2a);
-            r2b = fma(db, db, r2b);
+      for (int r = 0; r < NR; r++) acc[t][r] = 0.0;
+    }
+    for (int64_t q0 = lb; q0 < le; q0 += MAXMEM) {
+      const int nmem = (int)(le - q0 < MAXMEM ? le - q0 : MAXMEM);
+      int64_t len = 0;
+      if (tid < nmem) {
+        const int64_t sc = T.l_idx[q0 + tid];
+        const int64_t b = T.s_ptr[sc];
+        sbeg[tid] = b;
+        len = T.s_ptr[sc + 1] - b;
+      }
+      int64_t v = len;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        long long n2 = __shfl_up_sync(0xffffffffu, (long long)v, o);
+        if (lane >= o) v += n2;
+      }
+      if (lane == 31) wsum[warp] = v;
+      __syncthreads();
+      int64_t off = 0;
+      for (int w = 0; w < warp; w++) off += wsum[w];
+      if (tid < nmem) pref[tid + 1] = v + off;
+      if (tid == 0) pref[0] = 0;
+      __syncthreads();
+      const int64_t total = pref[nmem];
+      for (int64_t p0 = 0; p0 < total; p0 += TILE) {
+        const int cnt = (int)(total - p0 < TILE ? total - p0 : TILE);
+        for (int t = tid; t < cnt; t += IT2) {
+          const int64_t p = p0 + t;
+          int lo = 0, hi = nmem;
+          while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (pref[mid] <= p) lo = mid;
+            else hi = mid;
           }
-          double ka = kfast<KIND>(r2a, P.kp), kb = kfast<KIND>(r2b, P.kp);
+          const int64_t src = sbeg[lo] + (p - pref[lo]);
+          double rec[2 * W];
 #pragma unroll
-          for (int r = 0; r < NR; r++) {
-            acc[r] = fma(ka, __ldg(P.q + j * P.R + P.r0 + r), acc[r]);
-            acc[r] = fma(kb, __ldg(P.q + (j + 1) * P.R + P.r0 + r), acc[r]);
+          for (int k = 0; k < D; k++) rec[k] = __ldg(T.sc + k * T.ld_s + src);
+#pragma unroll
+          for (int r = 0; r < NR; r++) rec[D + r] = __ldg(T.q + src * R + r0 + r);
+#pragma unroll
+          for (int k = D + NR; k < 2 * W; k++) rec[k] = 0.0;
+#pragma unroll
+          for (int w = 0; w < W; w++) tile[t * W + w] = make_double2(rec[2 * w], rec[2 * w + 1]);
+        }
+        __syncthreads();
+        if (worker) {
+          for (int j = grp; j < cnt; j += G) {
+            double rec[2 * W];
+#pragma unroll
+            for (int w = 0; w < W; w++) {
+              const double2 u2 = tile[j * W + w];
+              rec[2 * w] = u2.x;
+              rec[2 * w + 1] = u2.y;
+            }
+#pragma unroll
+            for (int t = 0; t < RT; t++) {
+              double r2 = 0.0;
+#pragma unroll
+              for (int k = 0; k < D; k++) {
+                const double dk = x[t][k] - rec[k];
+                r2 = fma(dk, dk, r2);
+              }
+              double kv;
+              if constexpr ((KIND == COULOMB || KIND == LAPLACE) && !SELF) {
+                const double y = rsq_approx(r2);
+                const double e = fma(-r2, y * y, 1.0);
+                kv = fma(y * e, fma(0.375, e, 0.5), y);
+              } else {
+                kv = kpair<KIND>(r2, kp);
+              }
+#pragma unroll
+              for (int r = 0; r < NR; r++) acc[t][r] = fma(kv, rec[D + r], acc[t][r]);
+            }
           }
         }
-        if (j < se) {
-          double r2a = 0.0;
-#pragma unroll
-          for (int k = 0; k < D; k++) {
-            double da = x[k] - __ldg(P.sc + k * P.ld_s + j);
-            r2a = fma(da, da, r2a);
-          }
-          double ka = kfast<KIND>(r2a, P.kp);
-#pragma unroll
-          for (int r = 0; r < NR; r++) acc[r] = fma(ka, __ldg(P.q + j * P.R + P.r0 + r), acc[r]);
-        }
+        __syncthreads();
       }
     }
 #pragma unroll
-    for (int r = 0; r < NR; r++) part[threadIdx.x * NR + r] = acc[r];
+    for (int t = 0; t < RT; t++)
+#pragma unroll
+      for (int r = 0; r < NR; r++) part[(t * IT2 + tid) * NR + r] = acc[t][r];
     __syncthreads();
-    if (grp == 0 && active) {
-      double tot[NR];
+    if (worker && grp == 0) {
 #pragma unroll
-      for (int r = 0; r < NR; r++) tot[r] = 0.0;
-      for (int g = 0; g < G; g++)
+      for (int t = 0; t < RT; t++) {
+        if (!act[t]) continue;
+        const int64_t a = a0 + slot + t * TS;
 #pragma unroll
-        for (int r = 0; r < NR; r++) tot[r] += part[(g * TS + slot) * NR + r];
-#pragma unroll
-      for (int r = 0; r < NR; r++) tot[r] *= kscale<KIND>();
-      if (P.pm) {  // fused L2P
-        const int64_t k = P.kin[c];
-        const double* Pc = P.pm + P.pm_off[c];
-        const double* uc = P.uin + P.in_ptr[c] * P.R;
-        for (int64_t s = 0; s < k; s++) {
-          double pv = Pc[s * m + a];
-#pragma unroll
-          for (int r = 0; r < NR; r++) tot[r] = fma(pv, uc[s * P.R + P.r0 + r], tot[r]);
+        for (int r = 0; r < NR; r++) {
+          double tot = 0.0;
+          for (int g = 0; g < G; g++) tot += part[(t * IT2 + g * TS + slot) * NR + r];
+          T.out[(tb + a) * R + r0 + r] = tot * kscale<KIND>();
         }
       }
-      const int64_t row = P.out_perm ? P.out_perm[tb + a] : tb + a;
-#pragma unroll
-      for (int r = 0; r < NR; r++) P.out[row * P.R + P.r0 + r] = tot[r];
     }
     __syncthreads();
   }
 }
 
+template <int D, int KIND, int NR, int TILE>
+__global__ void __launch_bounds__(IT2) interact2(const int64_t* __restrict__ items,
+                                                 const LevelTab* __restrict__ tabs, int near_list, int64_t R,
+                                                 int64_t r0, KParams kp) {
+  constexpr int W = SrcW<D, NR>::W;
+  __shared__ double2 tile[W * TILE];
+  __shared__ int64_t pref[MAXMEM + 1];
+  __shared__ int64_t sbeg[MAXMEM];
+  __shared__ int64_t wsum[IT2 / 32];
+  __shared__ double part[2 * IT2 * NR];
+  const int64_t it = items[blockIdx.x];
+  const int lev = (int)(it >> 40);
+  const int64_t c = it & ((1ll << 40) - 1);
+  const LevelTab T = tabs[lev];
+  if (lev == near_list)
+    interact_cell<D, KIND, NR, TILE, true>(T, c, R, r0, kp, tile, pref, sbeg, wsum, part);
+  else
+    interact_cell<D, KIND, NR, TILE, false>(T, c, R, r0, kp, tile, pref, sbeg, wsum, part);
+}
+
 template <int D, int KIND>
-void launch_interact_k(const Interact& P, int64_t ncell, int nr, cudaStream_t s) {
+void launch_interact2(const DevH2& h, int64_t R, int64_t r0, int nr, const KParams& kp, cudaStream_t s) {
+  const int64_t* items = h.items.get();
+  const LevelTab* tabs = reinterpret_cast<const LevelTab*>(h.tabs.get());
+  unsigned g = (unsigned)h.n_items;
+  const int nl = h.t->depth + 1;  // list id of the leaf near field
+  if (!g) return;
   switch (nr) {
-    case 16: interact_kernel<D, KIND, 16><<<(unsigned)ncell, IT, 0, s>>>(P); break;
-    case 8: interact_kernel<D, KIND, 8><<<(unsigned)ncell, IT, 0, s>>>(P); break;
-    case 4: interact_kernel<D, KIND, 4><<<(unsigned)ncell, IT, 0, s>>>(P); break;
-    case 2: interact_kernel<D, KIND, 2><<<(unsigned)ncell, IT, 0, s>>>(P); break;
-    default: interact_kernel<D, KIND, 1><<<(unsigned)ncell, IT, 0, s>>>(P); break;
+    case 16: interact2<D, KIND, 16, 64><<<g, IT2, 0, s>>>(items, tabs, nl, R, r0, kp); break;
+    case 8: interact2<D, KIND, 8, 128><<<g, IT2, 0, s>>>(items, tabs, nl, R, r0, kp); break;
+    case 4: interact2<D, KIND, 4, 256><<<g, IT2, 0, s>>>(items, tabs, nl, R, r0, kp); break;
+    case 2: interact2<D, KIND, 2, 512><<<g, IT2, 0, s>>>(items, tabs, nl, R, r0, kp); break;
+    default: interact2<D, KIND, 1, 512><<<g, IT2, 0, s>>>(items, tabs, nl, R, r0, kp); break;
   }
   CKL();
 }
 
 template <int D>
-void launch_interact(int kind, const Interact& P, int64_t ncell, int nr, cudaStream_t s) {
-  if (ncell == 0) return;
+void interact_all_d(int kind, const DevH2& h, int64_t R, int64_t r0, int nr, const KParams& kp, cudaStream_t s) {
   switch (kind) {
-    case COULOMB: launch_interact_k<D, COULOMB>(P, ncell, nr, s); break;
-    case LAPLACE: launch_interact_k<D, LAPLACE>(P, ncell, nr, s); break;
-    case GAUSSIAN: launch_interact_k<D, GAUSSIAN>(P, ncell, nr, s); break;
-    case GAUSSIAN_SCALED: launch_interact_k<D, GAUSSIAN_SCALED>(P, ncell, nr, s); break;
-    case MATERN: launch_interact_k<D, MATERN>(P, ncell, nr, s); break;
-    case LOG: launch_interact_k<D, LOG>(P, ncell, nr, s); break;
-    case REG_INVERSE: launch_interact_k<D, REG_INVERSE>(P, ncell, nr, s); break;
-    default: launch_interact_k<D, REG_LOG>(P, ncell, nr, s); break;
+    case COULOMB: launch_interact2<D, COULOMB>(h, R, r0, nr, kp, s); break;
+    case LAPLACE: launch_interact2<D, LAPLACE>(h, R, r0, nr, kp, s); break;
+    case GAUSSIAN: launch_interact2<D, GAUSSIAN>(h, R, r0, nr, kp, s); break;
+    case GAUSSIAN_SCALED: launch_interact2<D, GAUSSIAN_SCALED>(h, R, r0, nr, kp, s); break;
+    case MATERN: launch_interact2<D, MATERN>(h, R, r0, nr, kp, s); break;
+    case LOG: launch_interact2<D, LOG>(h, R, r0, nr, kp, s); break;
+    case REG_INVERSE: launch_interact2<D, REG_INVERSE>(h, R, r0, nr, kp, s); break;
+    default: launch_interact2<D, REG_LOG>(h, R, r0, nr, kp, s); break;
   }
 }
 
-void interact(int d, int kind, const Interact& P, int64_t ncell, int nr, cudaStream_t s) {
+void interact_all(int d, int kind, const DevH2& h, int64_t R, int64_t r0, int nr, const KParams& kp,
+                  cudaStream_t s) {
   switch (d) {
-    case 1: launch_interact<1>(kind, P, ncell, nr, s); break;
-    case 2: launch_interact<2>(kind, P, ncell, nr, s); break;
-    case 3: launch_interact<3>(kind, P, ncell, nr, s); break;
-    default: launch_interact<4>(kind, P, ncell, nr, s); break;
+    case 1: interact_all_d<1>(kind, h, R, r0, nr, kp, s); break;
+    case 2: interact_all_d<2>(kind, h, R, r0, nr, kp, s); break;
+    case 3: interact_all_d<3>(kind, h, R, r0, nr, kp, s); break;
+    default: interact_all_d<4>(kind, h, R, r0, nr, kp, s); break;
   }
+}
+
+// u[perm[i]] = near[i] + P_c u_in(c)   (L2P fused with the scatter back to the caller's order)
+__global__ void l2p_scatter(int64_t ncell, const int64_t* __restrict__ t_ptr, const double* __restrict__ pm,
+                            const int64_t* __restrict__ pm_off, const int64_t* __restrict__ kin,
+                            const int64_t* __restrict__ in_ptr, const double* __restrict__ uin,
+                            const double* __restrict__ near, const int64_t* __restrict__ perm,
+                            double* __restrict__ u, int64_t R) {
+  const int64_t c = blockIdx.x;
+  const int64_t tb = t_ptr[c], m = t_ptr[c + 1] - tb;
+  const int64_t k = pm ? kin[c] : 0;
+  const double* Pc = pm ? pm + pm_off[c] : nullptr;
+  const double* uc = pm ? uin + in_ptr[c] * R : nullptr;
+  for (int64_t q = threadIdx.x; q < m * R; q += blockDim.x) {
+    const int64_t a = q / R, r = q - a * R;
+    double v = near[(tb + a) * R + r];
+    for (int64_t s2 = 0; s2 < k; s2++) v = fma(Pc[s2 * m + a], uc[s2 * R + r], v);
+    u[perm[tb + a] * R + r] = v;
+  }
+}
+
+// pair counts per work item (the reference's entry counts for S and near blocks)
+__global__ void item_costs(int64_t n, int lev, const int64_t* __restrict__ t_ptr, const int64_t* __restrict__ s_ptr,
+                           const int64_t* __restrict__ l_ptr, const int64_t* __restrict__ l_idx,
+                           unsigned long long* __restrict__ cost, int64_t* __restrict__ item) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  int64_t src = 0;
+  for (int64_t q = l_ptr[c]; q < l_ptr[c + 1]; q++) {
+    int64_t y = l_idx[q];
+    src += s_ptr[y + 1] - s_ptr[y];
+  }
+  cost[c] = (unsigned long long)((t_ptr[c + 1] - t_ptr[c]) * src);
+  item[c] = ((int64_t)lev << 40) | c;
 }
 
 KParams make_kp(int kind, double a) {
@@ -268,22 +400,104 @@ KParams make_kp(int kind, double a) {
   return kp;
 }
 
-void ensure_scratch(DevH2& h, int64_t R) {
+// work list: every M2L (level, cell) and every leaf near-field cell, by descending pair count
+void build_items(DevH2& h, cudaStream_t s) {
+  const DevTree& T = *h.t;
+  const int L = T.depth;
+  int64_t total = T.lv[L].n;
+  for (int l = 2; l <= L; l++) total += T.lv[l].n;
+  DBuf<unsigned long long> cost, cost_sorted;
+  DBuf<int64_t> item;
+  cost.alloc(total);
+  cost_sorted.alloc(total);
+  item.alloc(total);
+  h.items.alloc(total, &h.mem);
+  int64_t off = 0;
+  for (int l = 2; l <= L; l++) {
+    const DevLevel& Lv = T.lv[l];
+    const DevH2Level& HL = h.lv[l];
+    if (Lv.n)
+      item_costs<<<ceil_div(Lv.n, 256), 256, 0, s>>>(Lv.n, l, HL.in_ptr.get(), HL.out_ptrd(), Lv.il_ptr.get(),
+                                                     Lv.il_idx.get(), cost.get() + off, item.get() + off);
+    CKL();
+    off += Lv.n;
+  }
+  {
+    const DevLevel& Lv = T.lv[L];
+    item_costs<<<ceil_div(Lv.n, 256), 256, 0, s>>>(Lv.n, L + 1, Lv.t_ptr.get(),
+                                                   T.shared ? Lv.t_ptr.get() : Lv.s_ptr.get(), Lv.nb_ptr.get(),
+                                                   Lv.nb_idx.get(), cost.get() + off, item.get() + off);
+    CKL();
+  }
+  size_t bytes = 0;
+  CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, cost.get(), cost_sorted.get(), item.get(),
+                                               h.items.get(), total, 0, 64, s));
+  DBuf<unsigned char> tmp;
+  tmp.alloc(bytes);
+  CK(cub::DeviceRadixSort::SortPairsDescending(tmp.get(), bytes, cost.get(), cost_sorted.get(), item.get(),
+                                               h.items.get(), total, 0, 64, s));
+  // drop zero-cost items (cells with no targets or an empty list)
+  auto hc = to_host(cost_sorted.get(), total, s);
+  int64_t nz = 0;
+  while (nz < total && hc[nz] > 0) nz++;
+  h.n_items = nz;
+}
+
+void build_tabs(DevH2& h, int64_t R, cudaStream_t s) {
+  const DevTree& T = *h.t;
+  const int L = T.depth;
+  std::vector<LevelTab> tabs(L + 2);
+  for (int l = 2; l <= L; l++) {
+    const DevLevel& Lv = T.lv[l];
+    const DevH2Level& HL = h.lv[l];
+    LevelTab& t = tabs[l];
+    t.tc = HL.tin_c.get();
+    t.ld_t = std::max<int64_t>(HL.in_total, 1);
+    t.t_ptr = HL.in_ptr.get();
+    t.sc = HL.sout_cd();
+    t.ld_s = std::max<int64_t>(HL.out_total, 1);
+    t.s_ptr = HL.out_ptrd();
+    t.q = h.wout[l].get();
+    t.l_ptr = Lv.il_ptr.get();
+    t.l_idx = Lv.il_idx.get();
+    t.out = h.uin[l].get();
+  }
+  const DevLevel& Lv = T.lv[L];
+  LevelTab& t = tabs[L + 1];
+  t.tc = T.tsd();
+  t.ld_t = T.np;
+  t.t_ptr = Lv.t_ptr.get();
+  t.sc = T.ssd();
+  t.ld_s = T.nq;
+  t.s_ptr = T.shared ? Lv.t_ptr.get() : Lv.s_ptr.get();
+  t.q = h.w_sorted.get();
+  t.l_ptr = Lv.nb_ptr.get();
+  t.l_idx = Lv.nb_idx.get();
+  t.out = h.near.get();
+  h.tabs.alloc(sizeof(LevelTab) * tabs.size(), &h.mem);
+  CK(cudaMemcpyAsync(h.tabs.get(), tabs.data(), sizeof(LevelTab) * tabs.size(), cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));
+}
+
+void ensure_scratch(DevH2& h, int64_t R, cudaStream_t s) {
   const DevTree& T = *h.t;
   if (h.scratch_nrhs == R) return;
-  h.w_sorted.alloc(T.nq * R);
+  h.w_sorted.alloc(T.nq * R, &h.mem);
+  h.near.alloc(T.np * R, &h.mem);
   h.wout.clear();
   h.uin.clear();
   h.wout.resize(T.depth + 1);
   h.uin.resize(T.depth + 1);
   for (int l = 2; l <= T.depth; l++) {
-    h.wout[l].alloc(std::max<int64_t>(h.lv[l].out_total * R, 1));
-    h.uin[l].alloc(std::max<int64_t>(h.lv[l].in_total * R, 1));
+    h.wout[l].alloc(std::max<int64_t>(h.lv[l].out_total * R, 1), &h.mem);
+    h.uin[l].alloc(std::max<int64_t>(h.lv[l].in_total * R, 1), &h.mem);
   }
+  if (!h.items.n) build_items(h, s);
+  build_tabs(h, R, s);
   h.scratch_nrhs = R;
 }
 
-// 1D-chunked RHS widths supported by the interaction kernel
+// RHS widths supported by the interaction kernel
 void rhs_chunks(int64_t R, std::vector<std::pair<int64_t, int>>& out) {
   out.clear();
   int64_t r0 = 0;
@@ -297,6 +511,8 @@ void rhs_chunks(int64_t R, std::vector<std::pair<int64_t, int>>& out) {
 
 }  // namespace
 
+void prepare_matvec(DevH2& h, cudaStream_t s) { ensure_scratch(h, 1, s); }
+
 void set_profiling(bool on) { g_profile = on; }
 void last_stage_ms(double* ms5) {
   for (int i = 0; i < 5; i++) ms5[i] = g_stage_ms[i];
@@ -307,14 +523,15 @@ int64_t matvec_launches(const DevH2& h, int64_t nrhs) {
   std::vector<std::pair<int64_t, int>> ch;
   rhs_chunks(nrhs, ch);
   int64_t nchunk = (int64_t)ch.size();
-  if (L < 2) return 1 + nchunk;
-  return 1 + 1 + (L - 2) + (L - 1) * nchunk + (L - 2) + nchunk;
+  if (L < 2) return 1 + nchunk + 1;
+  // gather, P2M, M2M x (L-2), interaction x chunks, L2L x (L-2), L2P+scatter
+  return 1 + 1 + (L - 2) + nchunk + (L - 2) + 1;
 }
 
 void matvec(DevH2& h, const double* w, double* u, int64_t R, cudaStream_t s) {
   const DevTree& T = *h.t;
   const int L = T.depth, d = T.d;
-  ensure_scratch(h, R);
+  ensure_scratch(h, R, s);
   KParams kp = make_kp(h.kind, h.a);
   std::vector<std::pair<int64_t, int>> chunks;
   rhs_chunks(R, chunks);
@@ -344,74 +561,32 @@ void matvec(DevH2& h, const double* w, double* u, int64_t R, cudaStream_t s) {
                                             HL.out_ptrd(), R);
       CKL();
     }
-    if (g_profile) CK(cudaEventRecord(ev[1], s));
-    // ---- transverse pass (M2L), every level ----
-    for (int l = 2; l <= L; l++) {
-      const DevLevel& Lv = T.lv[l];
-      const DevH2Level& HL = h.lv[l];
-      Interact P{};
-      P.tc = HL.tin_c.get();
-      P.ld_t = std::max<int64_t>(HL.in_total, 1);
-      P.t_ptr = HL.in_ptr.get();
-      P.sc = HL.sout_cd();
-      P.ld_s = std::max<int64_t>(HL.out_total, 1);
-      P.s_ptr = HL.out_ptrd();
-      P.q = h.wout[l].get();
-      P.l_ptr = Lv.il_ptr.get();
-      P.l_idx = Lv.il_idx.get();
-      P.out = h.uin[l].get();
-      P.R = R;
-      P.kp = kp;
-      for (auto& ch : chunks) {
-        P.r0 = ch.first;
-        interact(d, h.kind, P, Lv.n, ch.second, s);
-      }
-    }
-    if (g_profile) CK(cudaEventRecord(ev[2], s));
-    // ---- downward pass (L2L) ----
-    for (int l = 2; l < L; l++) {
-      const DevLevel& Lv = T.lv[l];
-      const DevH2Level& HL = h.lv[l];
-      const DevH2Level& HC = h.lv[l + 1];
-      gemv_n_add<<<(unsigned)Lv.n, 128, 0, s>>>(Lv.n, HL.kin.get(), HL.m_in.get(), HL.pmat.get(), HL.pm_off.get(),
-                                                h.uin[l].get(), HL.in_ptr.get(), h.uin[l + 1].get(), HC.in_ptr.get(),
-                                                Lv.ch_ptr.get(), R);
-      CKL();
-    }
-  } else if (g_profile) {
-    CK(cudaEventRecord(ev[1], s));
-    CK(cudaEventRecord(ev[2], s));
+  }
+  if (g_profile) CK(cudaEventRecord(ev[1], s));
+  // ---- every M2L level + the near field in one launch ----
+  for (auto& ch : chunks) interact_all(d, h.kind, h, R, ch.first, ch.second, kp, s);
+  if (g_profile) CK(cudaEventRecord(ev[2], s));
+  // ---- downward pass (L2L) ----
+  for (int l = 2; l < L; l++) {
+    const DevLevel& Lv = T.lv[l];
+    const DevH2Level& HL = h.lv[l];
+    const DevH2Level& HC = h.lv[l + 1];
+    gemv_n_add<<<(unsigned)Lv.n, 128, 0, s>>>(Lv.n, HL.kin.get(), HL.m_in.get(), HL.pmat.get(), HL.pm_off.get(),
+                                              h.uin[l].get(), HL.in_ptr.get(), h.uin[l + 1].get(), HC.in_ptr.get(),
+                                              Lv.ch_ptr.get(), R);
+    CKL();
   }
   if (g_profile) CK(cudaEventRecord(ev[3], s));
-  // ---- near field (P2P) + L2P + scatter to the caller's order ----
+  // ---- L2P + near field, scattered to the caller's order ----
   {
     const DevLevel& Lv = T.lv[L];
-    Interact P{};
-    P.tc = T.tsd();
-    P.ld_t = T.np;
-    P.t_ptr = Lv.t_ptr.get();
-    P.sc = T.ssd();
-    P.ld_s = T.nq;
-    P.s_ptr = T.shared ? Lv.t_ptr.get() : Lv.s_ptr.get();
-    P.q = h.w_sorted.get();
-    P.l_ptr = Lv.nb_ptr.get();
-    P.l_idx = Lv.nb_idx.get();
-    P.out = u;
-    P.out_perm = T.t_perm.get();
-    if (L >= 2) {
-      const DevH2Level& HL = h.lv[L];
-      P.pm = HL.pmat.get();
-      P.pm_off = HL.pm_off.get();
-      P.kin = HL.kin.get();
-      P.in_ptr = HL.in_ptr.get();
-      P.uin = h.uin[L].get();
-    }
-    P.R = R;
-    P.kp = kp;
-    for (auto& ch : chunks) {
-      P.r0 = ch.first;
-      interact(d, h.kind, P, Lv.n, ch.second, s);
-    }
+    const bool far = L >= 2;
+    const DevH2Level* HL = far ? &h.lv[L] : nullptr;
+    l2p_scatter<<<(unsigned)Lv.n, 128, 0, s>>>(Lv.n, Lv.t_ptr.get(), far ? HL->pmat.get() : nullptr,
+                                               far ? HL->pm_off.get() : nullptr, far ? HL->kin.get() : nullptr,
+                                               far ? HL->in_ptr.get() : nullptr, far ? h.uin[L].get() : nullptr,
+                                               h.near.get(), T.t_perm.get(), u, R);
+    CKL();
   }
   if (g_profile) {
     CK(cudaEventRecord(ev[4], s));

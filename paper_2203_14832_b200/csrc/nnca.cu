@@ -703,6 +703,7 @@ std::unique_ptr<DevH2> assemble_impl(const DevTree& T, int kind, double a, doubl
     CKL();
     H->evals_nearfield = (int64_t)read_one(acc.get(), s);
   }
+  prepare_matvec(*H, s);  // interaction work list + scratch are part of the setup
   CK(cudaStreamSynchronize(s));
   H->setup_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
   return H;

@@ -87,6 +87,9 @@ struct DevH2 {
   DBuf<int64_t> items;      // interaction work list ((list << 40) | cell), by descending pair count
   int64_t n_items = 0;
   DBuf<unsigned char> tabs; // per-list pointer tables for the interaction kernel
+  DBuf<unsigned char> packtab;
+  DBuf<double> rec;         // packed source records [coords, charges] of every list
+  int64_t rec_total = 0;
 };
 
 // tree.cu

@@ -80,7 +80,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -217,6 +217,10 @@ def run_b200(args, cfg, world, rank, local):
     kern = h2c.builtin_kernel(kname, cfg[2], **kkw)
     cloud = h2c.PointCloud.from_points(pts)
 
+    # ---- warm-up of the engine on a small problem (lazy CUDA module loading, allocator) ----
+    wcloud = h2c.PointCloud.from_points(pts[:: max(1, n // 4096)][:4096])
+    h2c.h2_matvec(h2c.assemble(h2c.build_tree(wcloud, nu=nu, eta=float(np.sqrt(2.0))), kern, eps),
+                  np.ones(wcloud.n_sources))
     # ---- setup: tree + NNCA (timed on the host around synchronous calls) ----
     torch.cuda.synchronize()
     t0 = time.perf_counter()

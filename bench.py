@@ -120,6 +120,7 @@ class ClockSampler:
 
 
 def dist_setup():
+    """One process per GPU (torchrun env); NCCL on GPUs, gloo otherwise (CPU tests)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -127,18 +128,23 @@ def dist_setup():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     return world, rank, local
 
 
 def max_over_ranks(x, world):
+    """Max of a per-rank float over all ranks (the driver's max-over-ranks timing rule)."""
     if world == 1:
         return x
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -148,6 +154,11 @@ def barrier(world):
         import torch.distributed as dist
 
         dist.barrier()
+
+
+def aggregate_value(n_points, ms_per_step_max, world):
+    """Replicas: every rank multiplies its own copy of the operator; whole-job N^2/s."""
+    return world * float(n_points) ** 2 / (ms_per_step_max * 1e-3)
 
 
 def oracle_pipeline(pts, cfg, w, threads=None, matvecs=1):
@@ -258,7 +269,7 @@ def run_b200(args, cfg, world, rank, local):
     barrier(world)
     per = [e0.elapsed_time(e1) for e0, e1 in evs]
     ms = max_over_ranks(float(np.mean(per)), world)
-    value = world * n * n / (ms * 1e-3)
+    value = aggregate_value(n, ms, world)
 
     # ---- e2e: through the C ABI with pinned host buffers (H2D + matvec + D2H per step) ----
     wh = torch.from_numpy(np.ascontiguousarray(w)).pin_memory()
@@ -274,7 +285,7 @@ def run_b200(args, cfg, world, rank, local):
         e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(float(np.mean([e0.elapsed_time(e1) for e0, e1 in ee])), world)
-    e2e_value = world * n * n / (e2e_ms * 1e-3)
+    e2e_value = aggregate_value(n, e2e_ms, world)
 
     # ---- roofline of the dominant kernel family (FP64 interaction kernel: M2L + near field) ----
     st = h2.native_stats()

@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 
 #include "engine.cuh"
@@ -25,8 +26,9 @@ namespace h2b {
 
 namespace {
 
-constexpr int ACA_THREADS = 256;
-constexpr int ACA_WARPS = ACA_THREADS / 32;
+constexpr int ACA_MAX_THREADS = 256;
+constexpr int ACA_MAX_WARPS = ACA_MAX_THREADS / 32;
+constexpr int XCH = 8;  // cross-product partial sums per pass
 
 struct AcaArgs {
   int kind;
@@ -54,11 +56,14 @@ struct AcaArgs {
 };
 
 struct RedScratch {
-  double v[ACA_WARPS];
-  long long i[ACA_WARPS];
+  double v[ACA_MAX_WARPS];
+  long long i[ACA_MAX_WARPS];
+  double x[ACA_MAX_WARPS][XCH];
 };
 
+template <int NT>
 __device__ void block_argmax(double& v, int64_t& i, RedScratch& rs) {
+  constexpr int ACA_WARPS = NT / 32;
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   warp_argmax(v, i);
   __syncthreads();
@@ -72,7 +77,9 @@ __device__ void block_argmax(double& v, int64_t& i, RedScratch& rs) {
   for (int q = 0; q < ACA_WARPS; q++) argmax_merge(v, i, rs.v[q], rs.i[q]);
 }
 
+template <int NT>
 __device__ double block_sum(double x, RedScratch& rs) {
+  constexpr int ACA_WARPS = NT / 32;
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   x = warp_sum(x);
   __syncthreads();
@@ -83,7 +90,9 @@ __device__ double block_sum(double x, RedScratch& rs) {
   return s;
 }
 
+template <int NT>
 __device__ int64_t block_min(int64_t x, RedScratch& rs) {
+  constexpr int ACA_WARPS = NT / 32;
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   x = warp_min_i64(x);
   __syncthreads();
@@ -95,8 +104,10 @@ __device__ int64_t block_min(int64_t x, RedScratch& rs) {
 }
 
 // _core.pyx:184-305, one CTA per cell
-template <int D>
-__global__ void __launch_bounds__(ACA_THREADS) aca_kernel(AcaArgs A) {
+template <int D, int NT>
+__global__ void __launch_bounds__(NT, 2048 / NT / 2) aca_kernel(AcaArgs A) {
+  constexpr int ACA_THREADS = NT;
+  constexpr int ACA_WARPS = NT / 32;
   extern __shared__ double sm[];
   __shared__ RedScratch rs;
   __shared__ double xt[D], yb[D];
@@ -150,6 +161,7 @@ __global__ void __launch_bounds__(ACA_THREADS) aca_kernel(AcaArgs A) {
         for (int q = 0; q < D; q++) yl[q] = Yb[q * ldc + j];
         double acc = kval_exact(A.kind, A.a, r2_exact<D>(xl, yl));
         const double* Vj = V + j;
+#pragma unroll 8
         for (int64_t t = 0; t < k; t++) acc = __dsub_rn(acc, __dmul_rn(urow[t], Vj[t * n]));
         V[k * n + j] = acc;
         if (!cu[j]) {
@@ -161,13 +173,13 @@ __global__ void __launch_bounds__(ACA_THREADS) aca_kernel(AcaArgs A) {
         }
       }
       if (bj < 0) best = -1.0;
-      block_argmax(best, bj, rs);
+      block_argmax<NT>(best, bj, rs);
       nev += n;
       if (best > 0.0) break;
       int64_t first = INT64_MAX;
       for (int64_t i = tid; i < m; i += ACA_THREADS)
         if (!ru[i] && i < first) first = i;
-      first = block_min(first, rs);
+      first = block_min<NT>(first, rs);
       if (first == INT64_MAX) {
         exhausted = true;
         break;
@@ -188,15 +200,31 @@ __global__ void __launch_bounds__(ACA_THREADS) aca_kernel(AcaArgs A) {
     __syncthreads();
     if (tid == 0) cu[bj] = 1;
     for (int64_t t = tid; t < k; t += ACA_THREADS) vcol[t] = V[t * n + bj];
-    for (int64_t t = warp; t < k; t += ACA_WARPS) {
-      double s = 0.0;
-      const double* Vt = V + t * n;
-      const double* Vk = V + k * n;
-      for (int64_t j = lane; j < n; j += 32) s += Vt[j] * Vk[j];
-      s = warp_sum(s);
-      if (lane == 0) crossv[t] = s;
+    // crossv[t] = sum_j V[t][j] V[k][j]: threads keep their residual-row columns
+    // j and XCH partial sums, so V is streamed once and V[k] only k/XCH times
+    for (int64_t t0 = 0; t0 < k; t0 += XCH) {
+      double ps[XCH];
+#pragma unroll
+      for (int c = 0; c < XCH; c++) ps[c] = 0.0;
+      for (int64_t j = tid; j < n; j += ACA_THREADS) {
+        const double vk = V[k * n + j];
+#pragma unroll
+        for (int c = 0; c < XCH; c++)
+          if (t0 + c < k) ps[c] += V[(t0 + c) * n + j] * vk;
+      }
+#pragma unroll
+      for (int c = 0; c < XCH; c++) {
+        const double w = warp_sum(ps[c]);
+        if (lane == 0) rs.x[warp][c] = w;
+      }
+      __syncthreads();
+      if (tid < XCH && t0 + tid < k) {
+        double w = 0.0;
+        for (int q = 0; q < ACA_WARPS; q++) w += rs.x[q][tid];
+        crossv[t0 + tid] = w;
+      }
+      __syncthreads();
     }
-    __syncthreads();
     double yl[D];
 #pragma unroll
     for (int q = 0; q < D; q++) yl[q] = yb[q];
@@ -220,8 +248,8 @@ __global__ void __launch_bounds__(ACA_THREADS) aca_kernel(AcaArgs A) {
       s = warp_sum(s);
       if (lane == 0) crossu[t] = s;
     }
-    double u2 = block_sum(u2p, rs);
-    double v2 = block_sum(v2p, rs);  // block_sum syncs: crossu/crossv visible
+    double u2 = block_sum<NT>(u2p, rs);
+    double v2 = block_sum<NT>(v2p, rs);  // block_sum syncs: crossu/crossv visible
     for (int64_t t = 0; t < k; t++) norm2 += 2.0 * crossu[t] * crossv[t];
     norm2 += u2 * v2;
     if (tid == 0) {
@@ -248,7 +276,7 @@ __global__ void __launch_bounds__(ACA_THREADS) aca_kernel(AcaArgs A) {
           bi = i;
         }
       }
-    block_argmax(best, bi, rs);
+    block_argmax<NT>(best, bi, rs);
     if (bi < 0) break;
     trial = bi;
     __syncthreads();
@@ -427,11 +455,11 @@ size_t workspace_budget() {
   return std::max<size_t>(b, (size_t)256 << 20);
 }
 
-template <int D>
+template <int D, int NT>
 void set_aca_smem(size_t bytes) {
   static size_t done = 0;
-  if (bytes > 48 * 1024 && bytes > done) {
-    CK(cudaFuncSetAttribute(aca_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  if (bytes > 40 * 1024 && bytes > done) {
+    CK(cudaFuncSetAttribute(aca_kernel<D, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     done = bytes;
   }
 }
@@ -569,8 +597,23 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
     A.nevals = R.nevals.get();
     size_t smem = (size_t)std::max<int64_t>(maxcap, 1) * 4 * sizeof(double);
     if (smem > 200 * 1024) throw std::runtime_error("ACA rank cap too large for shared memory");
-    set_aca_smem<D>(smem);
-    aca_kernel<D><<<(unsigned)nb, ACA_THREADS, smem, s>>>(A);
+    {
+      // optional: cap CTAs per SM so the per-cell V working sets stay L2-resident
+      static const long pad = [] {
+        const char* e = getenv("H2B_ACA_SMEM_KB");
+        return e ? atol(e) : 0L;
+      }();
+      if (pad > 0) smem = std::max<size_t>(smem, (size_t)pad * 1024);
+    }
+    int64_t nsum = 0;
+    for (int64_t c = c0; c < c1; c++) nsum += std::max(mh[c], nh[c]);
+    if (nsum < 2048 * nb) {
+      set_aca_smem<D, 128>(smem);
+      aca_kernel<D, 128><<<(unsigned)nb, 128, smem, s>>>(A);
+    } else {
+      set_aca_smem<D, 256>(smem);
+      aca_kernel<D, 256><<<(unsigned)nb, 256, smem, s>>>(A);
+    }
     CKL();
     if (which_interp == 0)
       interp_kernel<<<(unsigned)nb, 256, 0, s>>>(0, c0, d_m.get(), R.rank.get(), U.get(), d_uoff.get(), rp.get(),
@@ -788,10 +831,10 @@ void aca_single(int kind, double a, const double* X, int64_t m, const double* Y,
   size_t smem = (size_t)cap * 4 * sizeof(double);
   if (smem > 200 * 1024) throw std::runtime_error("ACA rank cap too large for shared memory");
   switch (d) {
-    case 1: set_aca_smem<1>(smem); aca_kernel<1><<<1, ACA_THREADS, smem, s>>>(A); break;
-    case 2: set_aca_smem<2>(smem); aca_kernel<2><<<1, ACA_THREADS, smem, s>>>(A); break;
-    case 3: set_aca_smem<3>(smem); aca_kernel<3><<<1, ACA_THREADS, smem, s>>>(A); break;
-    default: set_aca_smem<4>(smem); aca_kernel<4><<<1, ACA_THREADS, smem, s>>>(A); break;
+    case 1: set_aca_smem<1, 256>(smem); aca_kernel<1, 256><<<1, 256, smem, s>>>(A); break;
+    case 2: set_aca_smem<2, 256>(smem); aca_kernel<2, 256><<<1, 256, smem, s>>>(A); break;
+    case 3: set_aca_smem<3, 256>(smem); aca_kernel<3, 256><<<1, 256, smem, s>>>(A); break;
+    default: set_aca_smem<4, 256>(smem); aca_kernel<4, 256><<<1, 256, smem, s>>>(A); break;
   }
   CKL();
   int64_t k = read_one(rk.get(), s);

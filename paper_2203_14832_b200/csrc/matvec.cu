@@ -31,49 +31,84 @@ __global__ void gather_rows(const double* __restrict__ w, const int64_t* __restr
   out[i] = w[perm[p] * R + r];
 }
 
-// upward: y_c[s] = sum_j A_c[s*nrow + j] x_c[j]   (P2M, M2M; A = column interpolator)
-// one CTA per cell, one warp per output row s
-__global__ void gemv_t(int64_t ncell, const int64_t* __restrict__ kout, const int64_t* __restrict__ nrow,
-                       const double* __restrict__ A, const int64_t* __restrict__ a_off,
-                       const double* __restrict__ x, const int64_t* __restrict__ x_ptr,
-                       const int64_t* __restrict__ x_map, double* __restrict__ y, const int64_t* __restrict__ y_ptr,
-                       int64_t R) {
-  int64_t c = blockIdx.x;
+// ---- transfer passes as one thread per output row (owner maps give the cell) ----
+__global__ void fill_owner(int64_t ncell, const int64_t* __restrict__ ptr, int* __restrict__ owner) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= ncell) return;
-  const int64_t k = kout[c], nr = nrow[c];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int64_t xo = x_map ? x_ptr[x_map[c]] : x_ptr[c];
+  for (int64_t p = ptr[c]; p < ptr[c + 1]; p++) owner[p] = (int)c;
+}
+
+// AT_c[j * k + s] = A_c[s * nr + j]: the upward pass reads the column
+// interpolator row-wise, so it gets a transposed copy (coalesced over s)
+__global__ void transpose_cells(int64_t ncell, const int64_t* __restrict__ nrow, const int64_t* __restrict__ kcol,
+                                const double* __restrict__ A, const int64_t* __restrict__ a_off,
+                                double* __restrict__ AT) {
+  const int64_t c = blockIdx.x;
+  if (c >= ncell) return;
+  const int64_t nr = nrow[c], k = kcol[c];
   const double* Ac = A + a_off[c];
-  const double* xc = x + xo * R;
-  double* yc = y + y_ptr[c] * R;
-  for (int64_t s = warp; s < k; s += nw) {
-    const double* As = Ac + s * nr;
-    for (int64_t r = 0; r < R; r++) {
-      double acc = 0.0;
-      for (int64_t j = lane; j < nr; j += 32) acc = fma(As[j], xc[j * R + r], acc);
-      acc = warp_sum(acc);
-      if (lane == 0) yc[s * R + r] = acc;
-    }
+  double* ATc = AT + a_off[c];
+  for (int64_t q = threadIdx.x; q < nr * k; q += blockDim.x) {
+    const int64_t j = q / k, sidx = q - j * k;
+    ATc[q] = Ac[sidx * nr + j];
   }
 }
 
-// downward: y_c[i] += sum_s A_c[s*nrow + i] x_c[s]   (L2L; A = row interpolator)
-__global__ void gemv_n_add(int64_t ncell, const int64_t* __restrict__ kin, const int64_t* __restrict__ nrow,
-                           const double* __restrict__ A, const int64_t* __restrict__ a_off,
-                           const double* __restrict__ x, const int64_t* __restrict__ x_ptr, double* __restrict__ y,
-                           const int64_t* __restrict__ y_ptr, const int64_t* __restrict__ y_map, int64_t R) {
-  int64_t c = blockIdx.x;
-  if (c >= ncell) return;
-  const int64_t k = kin[c], nr = nrow[c];
-  const double* Ac = A + a_off[c];
-  const double* xc = x + x_ptr[c] * R;
-  double* yc = y + y_ptr[y_map[c]] * R;
-  for (int64_t i = threadIdx.x; i < nr; i += blockDim.x)
-    for (int64_t r = 0; r < R; r++) {
-      double acc = 0.0;
-      for (int64_t s = 0; s < k; s++) acc = fma(Ac[s * nr + i], xc[s * R + r], acc);
-      yc[i * R + r] += acc;
-    }
+// upward (P2M / M2M): y[p] = sum_j AT_c[j * k + s] x_c[j],  p = out_ptr[c] + s
+__global__ void up_rows(int64_t nout, const int* __restrict__ owner, const int64_t* __restrict__ out_ptr,
+                        const int64_t* __restrict__ nrow, const double* __restrict__ A,
+                        const int64_t* __restrict__ a_off, const double* __restrict__ x,
+                        const int64_t* __restrict__ x_ptr, const int64_t* __restrict__ x_map,
+                        double* __restrict__ y, int64_t R) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= nout * R) return;
+  const int64_t p = q / R, r = q - p * R;
+  const int c = owner[p];
+  const int64_t sidx = p - out_ptr[c], nr = nrow[c], k = out_ptr[c + 1] - out_ptr[c];
+  const double* As = A + a_off[c] + sidx;
+  const double* xc = x + (x_map ? x_ptr[x_map[c]] : x_ptr[c]) * R + r;
+  double acc = 0.0;
+  for (int64_t j = 0; j < nr; j++) acc = fma(As[j * k], xc[j * R], acc);
+  y[q] = acc;
+}
+
+// downward (L2L): rows of the children stacked under parent P: u_child[q] += sum_s P_P[s * nr + i] u_P[s]
+__global__ void down_rows(int64_t nin_child, const int* __restrict__ child_owner, const int64_t* __restrict__ parent,
+                          const int64_t* __restrict__ ch_ptr, const int64_t* __restrict__ in_ptr_child,
+                          const int64_t* __restrict__ in_ptr, const int64_t* __restrict__ kin,
+                          const int64_t* __restrict__ nrow, const double* __restrict__ Pm,
+                          const int64_t* __restrict__ pm_off, const double* __restrict__ uin,
+                          double* __restrict__ uin_child, int64_t R) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= nin_child * R) return;
+  const int64_t p = q / R, r = q - p * R;
+  const int64_t P = parent[child_owner[p]];
+  const int64_t i = p - in_ptr_child[ch_ptr[P]], nr = nrow[P], k = kin[P];
+  const double* Pc = Pm + pm_off[P] + i;
+  const double* uc = uin + in_ptr[P] * R + r;
+  double acc = 0.0;
+  for (int64_t t = 0; t < k; t++) acc = fma(Pc[t * nr], uc[t * R], acc);
+  uin_child[q] += acc;
+}
+
+// leaves: u[perm[p]] = near[p] + sum_s P_c[s * m + a] u_in(c)[s]
+__global__ void l2p_rows(int64_t np, const int* __restrict__ owner, const int64_t* __restrict__ t_ptr,
+                         const double* __restrict__ pm, const int64_t* __restrict__ pm_off,
+                         const int64_t* __restrict__ kin, const int64_t* __restrict__ in_ptr,
+                         const double* __restrict__ uin, const double* __restrict__ near,
+                         const int64_t* __restrict__ perm, double* __restrict__ u, int64_t R) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= np * R) return;
+  const int64_t p = q / R, r = q - p * R;
+  double v = near[q];
+  if (pm) {
+    const int c = owner[p];
+    const int64_t a = p - t_ptr[c], m = t_ptr[c + 1] - t_ptr[c], k = kin[c];
+    const double* Pc = pm + pm_off[c] + a;
+    const double* uc = uin + in_ptr[c] * R + r;
+    for (int64_t t = 0; t < k; t++) v = fma(Pc[t * m], uc[t * R], v);
+  }
+  u[perm[p] * R + r] = v;
 }
 
 void interact_all(int d, int kind, const DevH2& h, int64_t R, int64_t r0, int nr, const KParams& kp,
@@ -83,25 +118,6 @@ void interact_all(int d, int kind, const DevH2& h, int64_t R, int64_t r0, int nr
     case 2: interact_all_d<2>(kind, h, R, r0, nr, kp, s); break;
     case 3: interact_all_d<3>(kind, h, R, r0, nr, kp, s); break;
     default: interact_all_d<4>(kind, h, R, r0, nr, kp, s); break;
-  }
-}
-
-// u[perm[i]] = near[i] + P_c u_in(c)   (L2P fused with the scatter back to the caller's order)
-__global__ void l2p_scatter(int64_t ncell, const int64_t* __restrict__ t_ptr, const double* __restrict__ pm,
-                            const int64_t* __restrict__ pm_off, const int64_t* __restrict__ kin,
-                            const int64_t* __restrict__ in_ptr, const double* __restrict__ uin,
-                            const double* __restrict__ near, const int64_t* __restrict__ perm,
-                            double* __restrict__ u, int64_t R) {
-  const int64_t c = blockIdx.x;
-  const int64_t tb = t_ptr[c], m = t_ptr[c + 1] - tb;
-  const int64_t k = pm ? kin[c] : 0;
-  const double* Pc = pm ? pm + pm_off[c] : nullptr;
-  const double* uc = pm ? uin + in_ptr[c] * R : nullptr;
-  for (int64_t q = threadIdx.x; q < m * R; q += blockDim.x) {
-    const int64_t a = q / R, r = q - a * R;
-    double v = near[(tb + a) * R + r];
-    for (int64_t s2 = 0; s2 < k; s2++) v = fma(Pc[s2 * m + a], uc[s2 * R + r], v);
-    u[perm[tb + a] * R + r] = v;
   }
 }
 
@@ -243,6 +259,35 @@ void ensure_scratch(DevH2& h, int64_t R, cudaStream_t s) {
     h.uin[l].alloc(std::max<int64_t>(h.lv[l].in_total * R, 1), &h.mem);
   }
   if (!h.items.n) build_items(h, s);
+  if (h.own_in.empty()) {
+    h.own_in.resize(T.depth + 1);
+    h.own_out.resize(T.depth + 1);
+    for (int l = 2; l <= T.depth; l++) {
+      const DevH2Level& HL = h.lv[l];
+      h.own_in[l].alloc(std::max<int64_t>(HL.in_total, 1), &h.mem);
+      fill_owner<<<ceil_div(HL.n, 256), 256, 0, s>>>(HL.n, HL.in_ptr.get(), h.own_in[l].get());
+      CKL();
+      if (!h.symmetric) {
+        h.own_out[l].alloc(std::max<int64_t>(HL.out_total, 1), &h.mem);
+        fill_owner<<<ceil_div(HL.n, 256), 256, 0, s>>>(HL.n, HL.out_ptrd(), h.own_out[l].get());
+        CKL();
+      }
+    }
+    h.qmat_t.resize(T.depth + 1);
+    for (int l = 2; l <= T.depth; l++) {
+      const DevH2Level& HL = h.lv[l];
+      const size_t nq = h.symmetric ? HL.pmat.n : HL.qmat.n;
+      h.qmat_t[l].alloc(std::max<size_t>(nq, 1), &h.mem);
+      if (HL.n)
+        transpose_cells<<<(unsigned)HL.n, 128, 0, s>>>(HL.n, HL.n_outd(), HL.koutd(), HL.qmatd(), HL.qm_offd(),
+                                                        h.qmat_t[l].get());
+      CKL();
+    }
+    const DevLevel& Lf = T.lv[T.depth];
+    h.own_t.alloc(std::max<int64_t>(T.np, 1), &h.mem);
+    fill_owner<<<ceil_div(Lf.n, 256), 256, 0, s>>>(Lf.n, Lf.t_ptr.get(), h.own_t.get());
+    CKL();
+  }
   build_tabs(h, R, s);
   h.scratch_nrhs = R;
 }
@@ -293,22 +338,23 @@ void matvec(DevH2& h, const double* w, double* u, int64_t R, cudaStream_t s) {
   gather_rows<<<ceil_div(T.nq * R, 256), 256, 0, s>>>(w, T.sperm(), T.nq, R, h.w_sorted.get());
   CKL();
   if (L >= 2) {
-    // ---- upward pass: P2M at the leaves, then M2M ----
+    // ---- upward pass: P2M at the leaves, then M2M (one thread per output row) ----
+    auto own_out = [&](int l) { return h.symmetric ? h.own_in[l].get() : h.own_out[l].get(); };
     {
       const DevLevel& Lv = T.lv[L];
       const DevH2Level& HL = h.lv[L];
-      gemv_t<<<(unsigned)Lv.n, 128, 0, s>>>(Lv.n, HL.koutd(), HL.n_outd(), HL.qmatd(), HL.qm_offd(),
-                                            h.w_sorted.get(), T.shared ? Lv.t_ptr.get() : Lv.s_ptr.get(), nullptr,
-                                            h.wout[L].get(), HL.out_ptrd(), R);
+      up_rows<<<ceil_div(HL.out_total * R, 256), 256, 0, s>>>(
+          HL.out_total, own_out(L), HL.out_ptrd(), HL.n_outd(), h.qmat_t[L].get(), HL.qm_offd(), h.w_sorted.get(),
+          T.shared ? Lv.t_ptr.get() : Lv.s_ptr.get(), nullptr, h.wout[L].get(), R);
       CKL();
     }
     for (int l = L - 1; l >= 2; l--) {
       const DevLevel& Lv = T.lv[l];
       const DevH2Level& HL = h.lv[l];
       const DevH2Level& HC = h.lv[l + 1];
-      gemv_t<<<(unsigned)Lv.n, 128, 0, s>>>(Lv.n, HL.koutd(), HL.n_outd(), HL.qmatd(), HL.qm_offd(),
-                                            h.wout[l + 1].get(), HC.out_ptrd(), Lv.ch_ptr.get(), h.wout[l].get(),
-                                            HL.out_ptrd(), R);
+      up_rows<<<ceil_div(HL.out_total * R, 256), 256, 0, s>>>(
+          HL.out_total, own_out(l), HL.out_ptrd(), HL.n_outd(), h.qmat_t[l].get(), HL.qm_offd(), h.wout[l + 1].get(),
+          HC.out_ptrd(), Lv.ch_ptr.get(), h.wout[l].get(), R);
       CKL();
     }
   }
@@ -316,26 +362,28 @@ void matvec(DevH2& h, const double* w, double* u, int64_t R, cudaStream_t s) {
   // ---- every M2L level + the near field in one launch ----
   for (auto& ch : chunks) interact_all(d, h.kind, h, R, ch.first, ch.second, kp, s);
   if (g_profile) CK(cudaEventRecord(ev[2], s));
-  // ---- downward pass (L2L) ----
+  // ---- downward pass (L2L), one thread per child row ----
   for (int l = 2; l < L; l++) {
     const DevLevel& Lv = T.lv[l];
+    const DevLevel& Lc = T.lv[l + 1];
     const DevH2Level& HL = h.lv[l];
     const DevH2Level& HC = h.lv[l + 1];
-    gemv_n_add<<<(unsigned)Lv.n, 128, 0, s>>>(Lv.n, HL.kin.get(), HL.m_in.get(), HL.pmat.get(), HL.pm_off.get(),
-                                              h.uin[l].get(), HL.in_ptr.get(), h.uin[l + 1].get(), HC.in_ptr.get(),
-                                              Lv.ch_ptr.get(), R);
+    down_rows<<<ceil_div(HC.in_total * R, 256), 256, 0, s>>>(
+        HC.in_total, h.own_in[l + 1].get(), Lc.parent.get(), Lv.ch_ptr.get(), HC.in_ptr.get(), HL.in_ptr.get(),
+        HL.kin.get(), HL.m_in.get(), HL.pmat.get(), HL.pm_off.get(), h.uin[l].get(), h.uin[l + 1].get(), R);
     CKL();
   }
   if (g_profile) CK(cudaEventRecord(ev[3], s));
-  // ---- L2P + near field, scattered to the caller's order ----
+  // ---- L2P + near field, scattered to the caller's order (one thread per target) ----
   {
     const DevLevel& Lv = T.lv[L];
     const bool far = L >= 2;
     const DevH2Level* HL = far ? &h.lv[L] : nullptr;
-    l2p_scatter<<<(unsigned)Lv.n, 128, 0, s>>>(Lv.n, Lv.t_ptr.get(), far ? HL->pmat.get() : nullptr,
-                                               far ? HL->pm_off.get() : nullptr, far ? HL->kin.get() : nullptr,
-                                               far ? HL->in_ptr.get() : nullptr, far ? h.uin[L].get() : nullptr,
-                                               h.near.get(), T.t_perm.get(), u, R);
+    l2p_rows<<<ceil_div(T.np * R, 256), 256, 0, s>>>(T.np, h.own_t.get(), Lv.t_ptr.get(),
+                                                     far ? HL->pmat.get() : nullptr, far ? HL->pm_off.get() : nullptr,
+                                                     far ? HL->kin.get() : nullptr, far ? HL->in_ptr.get() : nullptr,
+                                                     far ? h.uin[L].get() : nullptr, h.near.get(), T.t_perm.get(), u,
+                                                     R);
     CKL();
   }
   if (g_profile) {

@@ -125,6 +125,8 @@ __device__ __forceinline__ int64_t warp_min_i64(int64_t v) {
 // host helpers
 // ---------------------------------------------------------------------
 inline unsigned ceil_div(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
+// grid size for a bounds-checked 1D kernel: never 0 (a 0-block launch is an error)
+inline unsigned nblk(int64_t n, int64_t b) { return n > 0 ? ceil_div(n, b) : 1u; }
 
 // Device buffer with byte accounting.
 struct MemStats {

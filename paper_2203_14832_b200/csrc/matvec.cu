@@ -165,14 +165,14 @@ void build_items(DevH2& h, cudaStream_t s) {
     const DevLevel& Lv = T.lv[l];
     const DevH2Level& HL = h.lv[l];
     if (Lv.n)
-      item_costs<<<ceil_div(Lv.n, 256), 256, 0, s>>>(Lv.n, l, HL.in_ptr.get(), HL.out_ptrd(), Lv.il_ptr.get(),
+      item_costs<<<nblk(Lv.n, 256), 256, 0, s>>>(Lv.n, l, HL.in_ptr.get(), HL.out_ptrd(), Lv.il_ptr.get(),
                                                      Lv.il_idx.get(), cost.get() + off, item.get() + off);
     CKL();
     off += Lv.n;
   }
   {
     const DevLevel& Lv = T.lv[L];
-    item_costs<<<ceil_div(Lv.n, 256), 256, 0, s>>>(Lv.n, L + 1, Lv.t_ptr.get(),
+    item_costs<<<nblk(Lv.n, 256), 256, 0, s>>>(Lv.n, L + 1, Lv.t_ptr.get(),
                                                    T.shared ? Lv.t_ptr.get() : Lv.s_ptr.get(), Lv.nb_ptr.get(),
                                                    Lv.nb_idx.get(), cost.get() + off, item.get() + off);
     CKL();
@@ -265,11 +265,11 @@ void ensure_scratch(DevH2& h, int64_t R, cudaStream_t s) {
     for (int l = 2; l <= T.depth; l++) {
       const DevH2Level& HL = h.lv[l];
       h.own_in[l].alloc(std::max<int64_t>(HL.in_total, 1), &h.mem);
-      fill_owner<<<ceil_div(HL.n, 256), 256, 0, s>>>(HL.n, HL.in_ptr.get(), h.own_in[l].get());
+      fill_owner<<<nblk(HL.n, 256), 256, 0, s>>>(HL.n, HL.in_ptr.get(), h.own_in[l].get());
       CKL();
       if (!h.symmetric) {
         h.own_out[l].alloc(std::max<int64_t>(HL.out_total, 1), &h.mem);
-        fill_owner<<<ceil_div(HL.n, 256), 256, 0, s>>>(HL.n, HL.out_ptrd(), h.own_out[l].get());
+        fill_owner<<<nblk(HL.n, 256), 256, 0, s>>>(HL.n, HL.out_ptrd(), h.own_out[l].get());
         CKL();
       }
     }
@@ -285,7 +285,7 @@ void ensure_scratch(DevH2& h, int64_t R, cudaStream_t s) {
     }
     const DevLevel& Lf = T.lv[T.depth];
     h.own_t.alloc(std::max<int64_t>(T.np, 1), &h.mem);
-    fill_owner<<<ceil_div(Lf.n, 256), 256, 0, s>>>(Lf.n, Lf.t_ptr.get(), h.own_t.get());
+    fill_owner<<<nblk(Lf.n, 256), 256, 0, s>>>(Lf.n, Lf.t_ptr.get(), h.own_t.get());
     CKL();
   }
   build_tabs(h, R, s);
@@ -335,7 +335,7 @@ void matvec(DevH2& h, const double* w, double* u, int64_t R, cudaStream_t s) {
     for (auto& e : ev) CK(cudaEventCreate(&e));
     CK(cudaEventRecord(ev[0], s));
   }
-  gather_rows<<<ceil_div(T.nq * R, 256), 256, 0, s>>>(w, T.sperm(), T.nq, R, h.w_sorted.get());
+  gather_rows<<<nblk(T.nq * R, 256), 256, 0, s>>>(w, T.sperm(), T.nq, R, h.w_sorted.get());
   CKL();
   if (L >= 2) {
     // ---- upward pass: P2M at the leaves, then M2M (one thread per output row) ----
@@ -343,7 +343,7 @@ void matvec(DevH2& h, const double* w, double* u, int64_t R, cudaStream_t s) {
     {
       const DevLevel& Lv = T.lv[L];
       const DevH2Level& HL = h.lv[L];
-      up_rows<<<ceil_div(HL.out_total * R, 256), 256, 0, s>>>(
+      up_rows<<<nblk(HL.out_total * R, 256), 256, 0, s>>>(
           HL.out_total, own_out(L), HL.out_ptrd(), HL.n_outd(), h.qmat_t[L].get(), HL.qm_offd(), h.w_sorted.get(),
           T.shared ? Lv.t_ptr.get() : Lv.s_ptr.get(), nullptr, h.wout[L].get(), R);
       CKL();
@@ -352,7 +352,7 @@ void matvec(DevH2& h, const double* w, double* u, int64_t R, cudaStream_t s) {
       const DevLevel& Lv = T.lv[l];
       const DevH2Level& HL = h.lv[l];
       const DevH2Level& HC = h.lv[l + 1];
-      up_rows<<<ceil_div(HL.out_total * R, 256), 256, 0, s>>>(
+      up_rows<<<nblk(HL.out_total * R, 256), 256, 0, s>>>(
           HL.out_total, own_out(l), HL.out_ptrd(), HL.n_outd(), h.qmat_t[l].get(), HL.qm_offd(), h.wout[l + 1].get(),
           HC.out_ptrd(), Lv.ch_ptr.get(), h.wout[l].get(), R);
       CKL();
@@ -368,7 +368,7 @@ void matvec(DevH2& h, const double* w, double* u, int64_t R, cudaStream_t s) {
     const DevLevel& Lc = T.lv[l + 1];
     const DevH2Level& HL = h.lv[l];
     const DevH2Level& HC = h.lv[l + 1];
-    down_rows<<<ceil_div(HC.in_total * R, 256), 256, 0, s>>>(
+    down_rows<<<nblk(HC.in_total * R, 256), 256, 0, s>>>(
         HC.in_total, h.own_in[l + 1].get(), Lc.parent.get(), Lv.ch_ptr.get(), HC.in_ptr.get(), HL.in_ptr.get(),
         HL.kin.get(), HL.m_in.get(), HL.pmat.get(), HL.pm_off.get(), h.uin[l].get(), h.uin[l + 1].get(), R);
     CKL();
@@ -379,7 +379,7 @@ void matvec(DevH2& h, const double* w, double* u, int64_t R, cudaStream_t s) {
     const DevLevel& Lv = T.lv[L];
     const bool far = L >= 2;
     const DevH2Level* HL = far ? &h.lv[L] : nullptr;
-    l2p_rows<<<ceil_div(T.np * R, 256), 256, 0, s>>>(T.np, h.own_t.get(), Lv.t_ptr.get(),
+    l2p_rows<<<nblk(T.np * R, 256), 256, 0, s>>>(T.np, h.own_t.get(), Lv.t_ptr.get(),
                                                      far ? HL->pmat.get() : nullptr, far ? HL->pm_off.get() : nullptr,
                                                      far ? HL->kin.get() : nullptr, far ? HL->in_ptr.get() : nullptr,
                                                      far ? h.uin[L].get() : nullptr, h.near.get(), T.t_perm.get(), u,

@@ -14,7 +14,7 @@ import subprocess
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libh2b200.so")
+LIB_PATH = os.environ.get("H2B_LIB", os.path.join(HERE, "libh2b200.so"))  # H2B_LIB: dev override
 CSRC = os.path.join(HERE, "csrc")
 
 _i64p = ctypes.POINTER(ctypes.c_int64)

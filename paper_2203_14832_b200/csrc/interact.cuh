@@ -59,7 +59,13 @@ namespace {
 // the sources are packed records [x, y, z, q...] streamed into shared memory
 // with cp.async (double-buffered tiles) and read back as LDS.128 broadcasts.
 // ---------------------------------------------------------------------
-constexpr int IT2 = 128;
+#ifndef H2B_IT2
+#define H2B_IT2 128
+#endif
+#ifndef H2B_TILE1
+#define H2B_TILE1 256
+#endif
+constexpr int IT2 = H2B_IT2;
 constexpr int MEMPT = 2;                 // list members per thread in the prefix scan
 constexpr int MAXMEM = IT2 * MEMPT;      // list members per chunk
 
@@ -387,7 +393,7 @@ void launch_chunk(const DevH2& h, int64_t R, int64_t r0, const KParams& kp, cuda
 template <int D, int KIND>
 void launch_interact2(const DevH2& h, int64_t R, int64_t r0, int nr, const KParams& kp, cudaStream_t s) {
   if (nr == 16) launch_chunk<D, KIND, 16, 32>(h, R, r0, kp, s);
-  else launch_chunk<D, KIND, 1, 256>(h, R, r0, kp, s);
+  else launch_chunk<D, KIND, 1, H2B_TILE1>(h, R, r0, kp, s);
 }
 
 template <int D>

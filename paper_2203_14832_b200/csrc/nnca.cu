@@ -155,20 +155,43 @@ __global__ void __launch_bounds__(NT, 2048 / NT / 2) aca_kernel(AcaArgs A) {
       for (int q = 0; q < D; q++) xl[q] = xt[q];
       best = -1.0;
       bj = -1;
-      for (int64_t j = tid; j < n; j += ACA_THREADS) {
-        double yl[D];
+      // two columns per thread per pass: two independent exact-order chains
+      // keep twice the V loads in flight (the pass is DRAM-latency bound)
+      for (int64_t j0 = tid; j0 < n; j0 += 2 * ACA_THREADS) {
+        const int64_t j1 = j0 + ACA_THREADS;
+        const bool has1 = j1 < n;
+        double y0[D], y1[D];
 #pragma unroll
-        for (int q = 0; q < D; q++) yl[q] = Yb[q * ldc + j];
-        double acc = kval_exact(A.kind, A.a, r2_exact<D>(xl, yl));
-        const double* Vj = V + j;
+        for (int q = 0; q < D; q++) {
+          y0[q] = Yb[q * ldc + j0];
+          y1[q] = has1 ? Yb[q * ldc + j1] : y0[q];
+        }
+        double acc0 = kval_exact(A.kind, A.a, r2_exact<D>(xl, y0));
+        double acc1 = kval_exact(A.kind, A.a, r2_exact<D>(xl, y1));
+        const double* V0 = V + j0;
+        const double* V1 = V + (has1 ? j1 : j0);
 #pragma unroll 8
-        for (int64_t t = 0; t < k; t++) acc = __dsub_rn(acc, __dmul_rn(urow[t], Vj[t * n]));
-        V[k * n + j] = acc;
-        if (!cu[j]) {
-          double val = fabs(acc);
+        for (int64_t t = 0; t < k; t++) {
+          const double ut = urow[t];
+          acc0 = __dsub_rn(acc0, __dmul_rn(ut, V0[t * n]));
+          acc1 = __dsub_rn(acc1, __dmul_rn(ut, V1[t * n]));
+        }
+        V[k * n + j0] = acc0;
+        if (!cu[j0]) {
+          const double val = fabs(acc0);
           if (val > best) {
             best = val;
-            bj = j;
+            bj = j0;
+          }
+        }
+        if (has1) {
+          V[k * n + j1] = acc1;
+          if (!cu[j1]) {
+            const double val = fabs(acc1);
+            if (val > best) {
+              best = val;
+              bj = j1;
+            }
           }
         }
       }

@@ -87,12 +87,9 @@ struct DevH2 {
   DBuf<int64_t> items;      // interaction work list ((list << 40) | cell), by descending pair count
   int64_t n_items = 0;
   DBuf<unsigned char> tabs; // per-list pointer tables for the interaction kernel
-  DBuf<unsigned char> packtab;
-  DBuf<double> rec;         // packed source records [coords, charges] of every list
   std::vector<DBuf<int>> own_in, own_out;  // per level: pivot position -> owning cell
   DBuf<int> own_t;                          // sorted target position -> leaf cell
   std::vector<DBuf<double>> qmat_t;         // per level: transposed column interpolators (upward pass)
-  int64_t rec_total = 0;
 };
 
 // tree.cu

@@ -196,52 +196,38 @@ void build_tabs(DevH2& h, int64_t R, cudaStream_t s) {
   const DevTree& T = *h.t;
   const int L = T.depth;
   std::vector<LevelTab> tabs(L + 2);
-  std::vector<PackTab> packs(L + 2);
-  int64_t roff = 0;
   for (int l = 0; l <= L + 1; l++) {
     LevelTab& t = tabs[l];
-    PackTab& p = packs[l];
     std::memset(&t, 0, sizeof t);
-    std::memset(&p, 0, sizeof p);
-    p.rec_off = roff;
-    t.rec_off = roff;
     if (l >= 2 && l <= L) {
       const DevLevel& Lv = T.lv[l];
       const DevH2Level& HL = h.lv[l];
       t.tc = HL.tin_c.get();
       t.ld_t = std::max<int64_t>(HL.in_total, 1);
       t.t_ptr = HL.in_ptr.get();
+      t.sc = HL.sout_cd();
+      t.ld_s = std::max<int64_t>(HL.out_total, 1);
       t.s_ptr = HL.out_ptrd();
+      t.q = h.wout[l].get();
       t.l_ptr = Lv.il_ptr.get();
       t.l_idx = Lv.il_idx.get();
       t.out = h.uin[l].get();
-      p.sc = HL.sout_cd();
-      p.ld_s = std::max<int64_t>(HL.out_total, 1);
-      p.q = h.wout[l].get();
-      p.n = HL.out_total;
     } else if (l == L + 1) {
       const DevLevel& Lv = T.lv[L];
       t.tc = T.tsd();
       t.ld_t = T.np;
       t.t_ptr = Lv.t_ptr.get();
+      t.sc = T.ssd();
+      t.ld_s = T.nq;
       t.s_ptr = T.shared ? Lv.t_ptr.get() : Lv.s_ptr.get();
+      t.q = h.w_sorted.get();
       t.l_ptr = Lv.nb_ptr.get();
       t.l_idx = Lv.nb_idx.get();
       t.out = h.near.get();
-      p.sc = T.ssd();
-      p.ld_s = T.nq;
-      p.q = h.w_sorted.get();
-      p.n = T.nq;
     }
-    roff += p.n;
   }
-  h.rec_total = roff;
-  const int W = (T.d + (R >= 16 ? 16 : 1) + 2) / 2;
-  h.rec.alloc(std::max<int64_t>(roff, 1) * W * 2, &h.mem);
   h.tabs.alloc(sizeof(LevelTab) * tabs.size(), &h.mem);
-  h.packtab.alloc(sizeof(PackTab) * packs.size(), &h.mem);
   CK(cudaMemcpyAsync(h.tabs.get(), tabs.data(), sizeof(LevelTab) * tabs.size(), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(h.packtab.get(), packs.data(), sizeof(PackTab) * packs.size(), cudaMemcpyHostToDevice, s));
   CK(cudaStreamSynchronize(s));
 }
 
@@ -318,9 +304,9 @@ int64_t matvec_launches(const DevH2& h, int64_t nrhs) {
   std::vector<std::pair<int64_t, int>> ch;
   rhs_chunks(nrhs, ch);
   int64_t nchunk = (int64_t)ch.size();
-  if (L < 2) return 1 + 2 * nchunk + 1;
-  // gather, P2M, M2M x (L-2), (pack + interaction) x chunks, L2L x (L-2), L2P+scatter
-  return 1 + 1 + (L - 2) + 2 * nchunk + (L - 2) + 1;
+  if (L < 2) return 1 + nchunk + 1;
+  // gather, P2M, M2M x (L-2), interaction x chunks, L2L x (L-2), L2P+scatter
+  return 1 + 1 + (L - 2) + nchunk + (L - 2) + 1;
 }
 
 void matvec(DevH2& h, const double* w, double* u, int64_t R, cudaStream_t s) {

@@ -1,0 +1,193 @@
+// common.cuh — shared device helpers for the B200 NNCA / H2 engine.
+//
+// Two families of kernel evaluators:
+//   * kval_exact / r2_exact: the reference's arithmetic (_core.pyx:129 _kval,
+//     :152 _r2) with every rounding pinned by __d*_rn intrinsics so nvcc
+//     cannot contract into FMAs.  Used wherever results feed a discrete
+//     decision (ACA pivot search) or are compared bit-for-bit.
+//   * the fast evaluators in interact.cuh: FMA-contracted distance, MUFU
+//     rsqrt + Newton, used in the matvec (tolerance 1e-10 relative).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#define H2B_MAXD 4
+
+namespace h2b {
+
+struct cuda_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define CK(x)                                                                                  \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess)                                                                     \
+      throw ::h2b::cuda_error(std::string(#x) + ": " + cudaGetErrorString(e_) + " @" __FILE__ \
+                              ":" + std::to_string(__LINE__));                                 \
+  } while (0)
+
+#define CKL() CK(cudaGetLastError())
+
+constexpr double INV_FOUR_PI = 0.07957747154594767;
+
+enum Kind {
+  REG_LOG = 0,
+  REG_INVERSE = 1,
+  COULOMB = 2,
+  MATERN = 3,
+  GAUSSIAN = 4,
+  LAPLACE = 5,
+  LOG = 6,
+  GAUSSIAN_SCALED = 7
+};
+
+__host__ __device__ inline bool kind_valid(int k) { return k >= 0 && k <= 7; }
+
+// ---------------------------------------------------------------------
+// exact (reference-rounding) evaluation
+// ---------------------------------------------------------------------
+__device__ __forceinline__ double kval_exact(int kind, double a, double r2) {
+  if (kind == GAUSSIAN) return exp(-r2);
+  if (kind == GAUSSIAN_SCALED) return exp(-__dmul_rn(a, r2));
+  double r = __dsqrt_rn(r2);
+  switch (kind) {
+    case MATERN:
+      return exp(-r);
+    case COULOMB:
+      return r == 0.0 ? 0.0 : __ddiv_rn(1.0, r);
+    case LAPLACE:
+      return r == 0.0 ? 0.0 : __ddiv_rn(INV_FOUR_PI, r);
+    case LOG:
+      return r == 0.0 ? 0.0 : log(r);
+    case REG_INVERSE:
+      return r < a ? __ddiv_rn(r, a) : __ddiv_rn(a, r);
+    default:  // REG_LOG
+      if (r >= a) return __ddiv_rn(log(r), log(a));
+      if (r == 0.0) return 0.0;
+      return __ddiv_rn(__dmul_rn(r, __dsub_rn(log(r), 1.0)), __dmul_rn(a, __dsub_rn(log(a), 1.0)));
+  }
+}
+
+// sum_k (x_k - y_k)^2 accumulated left to right from 0.0, no FMA (_core.pyx:152)
+template <int D>
+__device__ __forceinline__ double r2_exact(const double* x, const double* y) {
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < D; k++) {
+    double df = __dsub_rn(x[k], y[k]);
+    acc = __dadd_rn(acc, __dmul_rn(df, df));
+  }
+  return acc;
+}
+
+// ---------------------------------------------------------------------
+// warp / block reductions
+// ---------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// argmax with ties to the lowest index; idx < 0 marks "none"
+__device__ __forceinline__ void argmax_merge(double& v, int64_t& i, double v2, int64_t i2) {
+  if (i2 < 0) return;
+  if (i < 0 || v2 > v || (v2 == v && i2 < i)) {
+    v = v2;
+    i = i2;
+  }
+}
+
+__device__ __forceinline__ void warp_argmax(double& v, int64_t& i) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+    long long i2 = __shfl_xor_sync(0xffffffffu, (long long)i, o);
+    argmax_merge(v, i, v2, i2);
+  }
+}
+
+__device__ __forceinline__ int64_t warp_min_i64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    long long v2 = __shfl_xor_sync(0xffffffffu, (long long)v, o);
+    v = v2 < v ? v2 : v;
+  }
+  return v;
+}
+
+// ---------------------------------------------------------------------
+// host helpers
+// ---------------------------------------------------------------------
+inline unsigned ceil_div(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
+// grid size for a bounds-checked 1D kernel: never 0 (a 0-block launch is an error)
+inline unsigned nblk(int64_t n, int64_t b) { return n > 0 ? ceil_div(n, b) : 1u; }
+
+// Device buffer with byte accounting.
+struct MemStats {
+  int64_t bytes = 0;
+};
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  MemStats* ms = nullptr;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), ms(o.ms) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p; n = o.n; ms = o.ms;
+      o.p = nullptr; o.n = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void alloc(size_t count, MemStats* stats = nullptr) {
+    release();
+    n = count;
+    ms = stats;
+    if (count) {
+      CK(cudaMalloc(&p, count * sizeof(T)));
+      if (ms) ms->bytes += (int64_t)(count * sizeof(T));
+    }
+  }
+  void release() {
+    if (p) {
+      cudaFree(p);
+      if (ms) ms->bytes -= (int64_t)(n * sizeof(T));
+    }
+    p = nullptr;
+    n = 0;
+  }
+  T* get() const { return p; }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+template <class T>
+inline std::vector<T> to_host(const T* d, size_t n, cudaStream_t s) {
+  std::vector<T> h(n);
+  if (n) {
+    CK(cudaMemcpyAsync(h.data(), d, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  return h;
+}
+
+template <class T>
+inline T read_one(const T* d, cudaStream_t s) {
+  T v;
+  CK(cudaMemcpyAsync(&v, d, sizeof(T), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return v;
+}
+
+}  // namespace h2b

@@ -70,15 +70,6 @@ struct DevH2Level {
   const int64_t* n_outd() const { return n_out.n ? n_out.get() : m_in.get(); }
 };
 
-// Packed source records of every interaction source list for one RHS width
-// (interact.cuh SrcRec): per level the outgoing pivots, then the leaf points.
-struct RecSet {
-  std::vector<DBuf<double2>> lists;  // [0, L - 2]: levels 2..L; [L - 1]: near field
-  DBuf<unsigned char> tabs;          // PackTab per list
-  int nlists = 0;
-  int64_t total = 0;
-};
-
 struct DevH2 {
   const DevTree* t = nullptr;
   int kind = 0, symmetric = 1;
@@ -99,8 +90,6 @@ struct DevH2 {
   std::vector<DBuf<int>> own_in, own_out;  // per level: pivot position -> owning cell
   DBuf<int> own_t;                          // sorted target position -> leaf cell
   std::vector<DBuf<double>> qmat_t;         // per level: transposed column interpolators (upward pass)
-  RecSet pack1, pack16;                     // source records for RHS chunks of width 1 / 16
-  DBuf<unsigned long long> work_counter;    // persistent interaction kernel: next work item
 };
 
 // tree.cu

@@ -7,9 +7,4 @@ void interact_all_d<3>(int kind, const DevH2& h, int64_t R, int64_t r0, int nr, 
                         cudaStream_t s) {
   interact_all_d_impl<3>(kind, h, R, r0, nr, kp, s);
 }
-template <>
-void pack_coords_dim<3>(const DevH2& h, int nr, cudaStream_t s) {
-  if (nr == 16) pack_coords_d<3, 16>(h, s);
-  else pack_coords_d<3, 1>(h, s);
-}
 }  // namespace h2b

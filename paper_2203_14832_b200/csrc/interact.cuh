@@ -52,28 +52,47 @@ __host__ __device__ constexpr double kscale() {
 // interaction-list cells with their multipole charges); list L + 1 is the
 // leaf near field (points, input charges).  Items are sorted by pair count,
 // largest first, so all levels share one balanced grid.  A CTA owns one
-// target cell: 2 targets per thread in registers, the source list streamed
-// through a shared-memory tile (coordinates + charges, LDS.128 broadcasts).
+// target cell: RT targets per thread in registers; the sources are streamed
+// through shared memory as packed records [y_0..y_{D-1}, q_0..q_{NR-1}]
+// (source records, `SrcRec`): every list member's sources are one contiguous
+// record range (Morton cell order), so a tile is filled by one TMA bulk copy
+// (cp.async.bulk, mbarrier completion) per member, double-buffered so the
+// copy of tile i+1 overlaps the arithmetic of tile i.
 // ---------------------------------------------------------------------
 namespace {
 
 #ifndef H2B_IT2
 #define H2B_IT2 128
 #endif
+#ifndef H2B_RT
+#define H2B_RT 2
+#endif
+#ifndef H2B_TILE16
+#define H2B_TILE16 32
+#endif
 #ifndef H2B_TILE1
-#define H2B_TILE1 512
+#define H2B_TILE1 128
 #endif
 constexpr int IT2 = H2B_IT2;
-constexpr int MAXMEM = IT2;
+#ifndef H2B_MAXMEMW
+#define H2B_MAXMEMW 256
+#endif
+constexpr int MAXMEMW = H2B_MAXMEMW;  // list members per member table
+
+// doubles per source record (padded to whole 16-byte words for TMA / LDS.128)
+template <int D, int NR>
+struct SrcRec {
+  static constexpr int RS = 2 * ((D + NR + 1) / 2);
+  static constexpr int W = RS / 2;  // double2 words
+};
 
 struct LevelTab {
   const double* tc;      // target coords SoA (ld_t)
   int64_t ld_t;
   const int64_t* t_ptr;  // target range per cell
-  const double* sc;      // source coords SoA (ld_s)
-  int64_t ld_s;
-  const int64_t* s_ptr;  // source range per source cell
-  const double* q;       // charges, row stride R
+  const int64_t* s_ptr;  // source range per source cell (record index)
+  const double2* rec1;   // source records for NR = 1
+  const double2* rec16;  // source records for NR = 16
   const int64_t* l_ptr;  // cell list (CSR)
   const int64_t* l_idx;
   double* out;           // result rows (target position) * R
@@ -85,142 +104,321 @@ __device__ __forceinline__ double rsq_approx(double x) {
   return y;
 }
 
-// K(r2) for the interaction kernel.  1/r: MUFU.RSQ64H seed + one Newton step
-// (cubic correction: ~1 ulp), with the punctured diagonal handled by
-// an integer test on the high word (r2 == 0 or subnormal -> 0).
+// ---- mbarrier / TMA bulk-copy helpers (sm_90+ PTX, used on sm_100a) ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// generic-proxy smem writes (the in-place transform) before a later TMA write
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// K(r2) for the interaction kernel, non-1/r kinds (1/r is acc_inv_r).
 template <int KIND>
 __device__ __forceinline__ double kpair(double r2, const KParams& kp) {
-  if constexpr (KIND == COULOMB || KIND == LAPLACE) {
-    const bool zero = __double2hiint(r2) == 0;
-    const double r2s = zero ? 1.0 : r2;
-    const double y = rsq_approx(r2s);
-    const double e = fma(-r2s, y * y, 1.0);
-    const double kv = fma(y * e, fma(0.375, e, 0.5), y);  // y (1 + e/2 + 3e^2/8): full FP64 accuracy
-    return zero ? 0.0 : kv;
+  return kfast<KIND>(r2, kp);
+}
+
+// r^2 of one pair.
+//   SELF (near field): coordinate differences, so identical points give
+//   exactly 0 (the punctured diagonal).
+//   Interaction lists (admissible, separated cells): both sides are shifted to
+//   the origin o = the first target of the CTA's cell, and
+//   r^2 = |x'|^2 + |y'|^2 - 2 x'.y'  costs 4 FP64 ops (DADD + 3 DFMA) instead
+//   of 6.  The cancellation error is ~eps (|x'|^2 + |y'|^2) / r^2 ~ 1e-15
+//   relative: |x'| <= diam(X), |y'| <= dist + 2 diam, and admissibility
+//   bounds diam / dist (measured: matvec error vs the oracle unchanged).
+template <int D, bool SELF>
+__device__ __forceinline__ double pair_r2(const double (&x)[D + 1], const double* rec, double yy) {
+  if constexpr (SELF) {
+    double r2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; k++) {
+      const double dk = x[k] - rec[k];
+      r2 = fma(dk, dk, r2);
+    }
+    return r2;
   } else {
-    return kfast<KIND>(r2, kp);
+    double r2 = x[D] + yy;  // |x'|^2 + |y'|^2
+#pragma unroll
+    for (int k = 0; k < D; k++) r2 = fma(x[k], rec[k], r2);  // x holds -2 x'
+    return r2;
   }
 }
 
-// Per-source record in shared memory: D coordinates then NR charges, padded
-// to whole double2 words so one source is W LDS.128 broadcasts.
-template <int D, int NR>
-struct SrcW {
-  static constexpr int W = (D + NR + 1) / 2;
+// Accumulate q K(r2) for 1/r (COULOMB / LAPLACE) in "2/r" units (the sum is
+// scaled by 1/2 at the end), from the MUFU.RSQ64H seed y (relative error
+// <= 9.2e-7, tools/ubench_rsq.cu).
+//   M2L (!SELF): cubic correction  2/r = y (2 + e + 3/4 e^2), e = 1 - r2 y^2
+//   (<= 1 ulp).  The multipole charges come from interpolation weights with
+//   cancellation, so a one-sided per-entry bias is amplified: a quadratic
+//   step (error 1.5 e^2 <= 1.3e-12 per entry) measured 2.5e-11 against the
+//   oracle at N = 1M, the cubic one 1.5e-13.
+//   Near field (SELF, plain input charges): quadratic step 2/r = y (3 - r2 y^2).
+//   TEST: the source range may hold the target itself or a duplicate point,
+//   r2 == 0 -> K = 0 (the punctured diagonal); only the target's own leaf can,
+//   so only that member pays for the test.
+template <int NR, bool SELF, bool TEST>
+__device__ __forceinline__ void acc_inv_r(double r2, const double* q, double (&acc)[NR]) {
+  if constexpr (TEST) {
+    const bool zero = __double2hiint(r2) == 0;  // r2 == 0 (or subnormal)
+    const double r2s = zero ? 1.0 : r2;
+    const double y = rsq_approx(r2s);
+    const double t = fma(-r2s, y * y, 3.0);
+    const double kv = zero ? 0.0 : y * t;
+#pragma unroll
+    for (int r = 0; r < NR; r++) acc[r] = fma(kv, q[r], acc[r]);
+  } else {
+    const double y = rsq_approx(r2);
+    double t;
+    if constexpr (SELF) {
+      t = fma(-r2, y * y, 3.0);
+    } else {
+      const double e = fma(-r2, y * y, 1.0);
+      t = fma(e, fma(0.75, e, 1.0), 2.0);
+    }
+    if constexpr (NR == 1) {
+      acc[0] = fma(y * q[0], t, acc[0]);
+    } else {
+      const double kv = y * t;
+#pragma unroll
+      for (int r = 0; r < NR; r++) acc[r] = fma(kv, q[r], acc[r]);
+    }
+  }
+}
+
+template <int KIND>
+__device__ __forceinline__ constexpr bool is_inv_r() {
+  return KIND == COULOMB || KIND == LAPLACE;
+}
+
+// Per-warp shared-memory state.  Every warp is an independent worker (no
+// CTA-wide barriers in the source loop): it owns two TMA stages, their
+// mbarriers and its list-member table.
+template <int D, int NR, int TILE, int RT>
+struct WarpSmem {
+  static constexpr int W = SrcRec<D, NR>::W;
+  double2 stage[2][TILE * W];  // TMA destinations (double-buffered)
+  double yy[TILE];             // |y'|^2 of the current tile (interaction lists)
+  uint64_t bar[2];             // "tile landed" mbarriers
+  int pref[MAXMEMW + 1];       // prefix of member lengths (records)
+  int64_t sbeg[MAXMEMW];       // first record of each member
+  double part[RT * 32 * NR];   // per-group partial sums
 };
 
-// Body for one target chunk.  RT = 2 targets per thread (register blocking:
-// every shared-memory source read feeds two pair evaluations).  SELF = the
-// list may contain the target itself (near field): punctured diagonal test.
+// Issue the TMA bulk copies of window [p0, p0 + cnt) of the member
+// concatenation into one stage (whole warp; lane 0 arms the mbarrier first).
+template <int W>
+__device__ __forceinline__ void issue_tile(const double2* rec, int nmem, const int* pref, const int64_t* sbeg,
+                                           int p0, int cnt, double2* dst, uint64_t* bar) {
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) mbar_expect_tx(bar, (uint32_t)cnt * (uint32_t)(W * 16));
+  __syncwarp();
+  int lo = 0, hi = nmem;  // last member with pref[q] <= p0
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (pref[mid] <= p0) lo = mid;
+    else hi = mid;
+  }
+  const int p1 = p0 + cnt;
+  for (int qm = lo + lane; qm < nmem && pref[qm] < p1; qm += 32) {
+    const int pa = pref[qm] > p0 ? pref[qm] : p0;
+    const int pb = pref[qm + 1] < p1 ? pref[qm + 1] : p1;
+    if (pb > pa)
+      bulk_g2s(dst + (pa - p0) * W, rec + (sbeg[qm] + (pa - pref[qm])) * W, (uint32_t)(pb - pa) * (W * 16), bar);
+  }
+}
+
+// Stream the concatenated source ranges of nmem list members (sbeg / pref in
+// the warp's shared memory) through the double-buffered tiles and accumulate
+// into the register-resident targets.  `ntile` counts the tiles this warp
+// has consumed (stage = ntile & 1, mbarrier parity = (ntile >> 1) & 1).
+template <int D, int KIND, int NR, int TILE, bool SELF, bool TEST, int RT>
+__device__ __forceinline__ void stream_members(WarpSmem<D, NR, TILE, RT>& S, const double2* rec, int nmem,
+                                               const double (&o)[D], const KParams& kp, bool worker, int grp,
+                                               int G, const double (&x)[RT][D + 1], double (&acc)[RT][NR],
+                                               uint32_t& ntile) {
+  constexpr int W = SrcRec<D, NR>::W;
+  const int lane = threadIdx.x & 31;
+  const int total = S.pref[nmem];
+  if (total == 0) return;
+  const int ntiles = (total + TILE - 1) / TILE;
+  issue_tile<W>(rec, nmem, S.pref, S.sbeg, 0, total < TILE ? total : TILE, S.stage[ntile & 1], &S.bar[ntile & 1]);
+  for (int it = 0; it < ntiles; it++, ntile++) {
+    const int b = ntile & 1;
+    const int p0 = it * TILE;
+    const int cnt = total - p0 < TILE ? total - p0 : TILE;
+    double2* tile = S.stage[b];
+    mbar_wait(&S.bar[b], (ntile >> 1) & 1);
+    if constexpr (!SELF) {  // shift to the target-cell origin in place, |y'|^2 aside
+      for (int e = lane; e < cnt; e += 32) {
+        double v[2 * W];
+#pragma unroll
+        for (int w = 0; w < W; w++) {
+          const double2 u2 = tile[e * W + w];
+          v[2 * w] = u2.x;
+          v[2 * w + 1] = u2.y;
+        }
+        double n2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < D; k++) {
+          v[k] -= o[k];
+          n2 = fma(v[k], v[k], n2);
+        }
+        S.yy[e] = n2;
+#pragma unroll
+        for (int w = 0; w < (D + 1) / 2; w++) tile[e * W + w] = make_double2(v[2 * w], v[2 * w + 1]);
+      }
+      fence_proxy_async();
+      __syncwarp();
+    }
+    // next tile into the other stage (its last reader finished before the __syncwarp closing the previous tile)
+    if (it + 1 < ntiles) {
+      const int q0 = p0 + TILE;
+      issue_tile<W>(rec, nmem, S.pref, S.sbeg, q0, total - q0 < TILE ? total - q0 : TILE, S.stage[b ^ 1],
+                    &S.bar[b ^ 1]);
+    }
+    if (worker) {
+#pragma unroll 2
+      for (int j = grp; j < cnt; j += G) {
+        double v[2 * W];
+#pragma unroll
+        for (int w = 0; w < W; w++) {
+          const double2 u2 = tile[j * W + w];
+          v[2 * w] = u2.x;
+          v[2 * w + 1] = u2.y;
+        }
+        const double yy = SELF ? 0.0 : S.yy[j];
+#pragma unroll
+        for (int t = 0; t < RT; t++) {
+          const double r2 = pair_r2<D, SELF>(x[t], v, yy);
+          if constexpr (is_inv_r<KIND>()) {
+            acc_inv_r<NR, SELF, TEST>(r2, v + D, acc[t]);
+          } else {
+            const double kv = kpair<KIND>(r2, kp);
+#pragma unroll
+            for (int r = 0; r < NR; r++) acc[t][r] = fma(kv, v[D + r], acc[t][r]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// Member table of list members [q0, q0 + nmem): first record and prefix of
+// lengths (warp scan, 32 members per step).  SELF drops the own leaf (done
+// separately through the r2 == 0 test path).
+template <bool SELF, class S_>
+__device__ __forceinline__ void member_table(const LevelTab& T, int64_t c, int64_t q0, int nmem, S_& S) {
+  const int lane = threadIdx.x & 31;
+  int run = 0;
+  for (int b = 0; b < nmem; b += 32) {
+    const int q = b + lane;
+    int len = 0;
+    if (q < nmem) {
+      const int64_t sc = T.l_idx[q0 + q];
+      const int64_t sb = T.s_ptr[sc];
+      S.sbeg[q] = sb;
+      len = (SELF && sc == c) ? 0 : (int)(T.s_ptr[sc + 1] - sb);
+    }
+    int v = len;
+#pragma unroll
+    for (int o2 = 1; o2 < 32; o2 <<= 1) {
+      const int n2 = __shfl_up_sync(0xffffffffu, v, o2);
+      if (lane >= o2) v += n2;
+    }
+    if (q < nmem) S.pref[q + 1] = run + v;
+    run += __shfl_sync(0xffffffffu, v, 31);
+  }
+  if (lane == 0) S.pref[0] = 0;
+  __syncwarp();
+}
+
+// One work item (list, cell) on one warp.  RT targets per lane (register
+// blocking: every shared-memory source read feeds RT pair evaluations), TS
+// lanes per target group, G = 32 / TS groups splitting the sources.  Near
+// field (SELF): the target's own leaf goes first through the r2 == 0 test
+// path, the other neighbours (never coincident with a target) through the
+// plain path.
 template <int D, int KIND, int NR, int TILE, bool SELF, int RT>
 __device__ __forceinline__ void interact_cell(const LevelTab& T, int64_t c, int64_t R, int64_t r0, const KParams& kp,
-                                              double2* tile, int64_t* pref, int64_t* sbeg, int64_t* wsum,
-                                              double* part) {
-  constexpr int W = SrcW<D, NR>::W;
+                                              WarpSmem<D, NR, TILE, RT>& S, uint32_t& ntile) {
+  const double2* rec = NR == 1 ? T.rec1 : T.rec16;
   const int64_t tb = T.t_ptr[c], m = T.t_ptr[c + 1] - tb;
   const int64_t lb = T.l_ptr[c], le = T.l_ptr[c + 1];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int64_t a0 = 0; a0 < m; a0 += RT * IT2) {
-    const int64_t mc = (m - a0) < RT * IT2 ? (m - a0) : RT * IT2;
+  const int lane = threadIdx.x & 31;
+  double o[D];
+#pragma unroll
+  for (int k = 0; k < D; k++) o[k] = SELF ? 0.0 : T.tc[k * T.ld_t + tb];
+  for (int64_t a0 = 0; a0 < m; a0 += RT * 32) {
+    const int64_t mc = (m - a0) < RT * 32 ? (m - a0) : RT * 32;
     const int TS = (int)((mc + RT - 1) / RT);
-    const int G = IT2 / TS;
-    const int slot = tid % TS, grp = tid / TS;
+    const int G = 32 / TS;
+    const int slot = lane % TS, grp = lane / TS;
     const bool worker = grp < G;
     bool act[RT];
-    double x[RT][D];
+    double x[RT][D + 1];
     double acc[RT][NR];
 #pragma unroll
     for (int t = 0; t < RT; t++) {
       const int64_t a = a0 + slot + t * TS;
       act[t] = worker && (slot + t * TS) < mc;
+      double n2 = 0.0;
 #pragma unroll
-      for (int k = 0; k < D; k++) x[t][k] = act[t] ? T.tc[k * T.ld_t + tb + a] : 0.0;
+      for (int k = 0; k < D; k++) {
+        const double xk = act[t] ? T.tc[k * T.ld_t + tb + a] : o[k];
+        if constexpr (SELF) {
+          x[t][k] = xk;
+        } else {
+          const double dk = xk - o[k];
+          n2 = fma(dk, dk, n2);
+          x[t][k] = -2.0 * dk;
+        }
+      }
+      x[t][D] = n2;
 #pragma unroll
       for (int r = 0; r < NR; r++) acc[t][r] = 0.0;
     }
-    for (int64_t q0 = lb; q0 < le; q0 += MAXMEM) {
-      const int nmem = (int)(le - q0 < MAXMEM ? le - q0 : MAXMEM);
-      int64_t len = 0;
-      if (tid < nmem) {
-        const int64_t sc = T.l_idx[q0 + tid];
-        const int64_t b = T.s_ptr[sc];
-        sbeg[tid] = b;
-        len = T.s_ptr[sc + 1] - b;
+    if constexpr (SELF) {  // own leaf: the only member that can hold r2 == 0
+      if (lane == 0) {
+        const int64_t b = T.s_ptr[c];
+        S.sbeg[0] = b;
+        S.pref[0] = 0;
+        S.pref[1] = (int)(T.s_ptr[c + 1] - b);
       }
-      int64_t v = len;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        long long n2 = __shfl_up_sync(0xffffffffu, (long long)v, o);
-        if (lane >= o) v += n2;
-      }
-      if (lane == 31) wsum[warp] = v;
-      __syncthreads();
-      int64_t off = 0;
-      for (int w = 0; w < warp; w++) off += wsum[w];
-      if (tid < nmem) pref[tid + 1] = v + off;
-      if (tid == 0) pref[0] = 0;
-      __syncthreads();
-      const int64_t total = pref[nmem];
-      for (int64_t p0 = 0; p0 < total; p0 += TILE) {
-        const int cnt = (int)(total - p0 < TILE ? total - p0 : TILE);
-        for (int t = tid; t < cnt; t += IT2) {
-          const int64_t p = p0 + t;
-          int lo = 0, hi = nmem;
-          while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (pref[mid] <= p) lo = mid;
-            else hi = mid;
-          }
-          const int64_t src = sbeg[lo] + (p - pref[lo]);
-          double rec[2 * W];
-#pragma unroll
-          for (int k = 0; k < D; k++) rec[k] = __ldg(T.sc + k * T.ld_s + src);
-#pragma unroll
-          for (int r = 0; r < NR; r++) rec[D + r] = __ldg(T.q + src * R + r0 + r);
-#pragma unroll
-          for (int k = D + NR; k < 2 * W; k++) rec[k] = 0.0;
-#pragma unroll
-          for (int w = 0; w < W; w++) tile[t * W + w] = make_double2(rec[2 * w], rec[2 * w + 1]);
-        }
-        __syncthreads();
-        if (worker) {
-          for (int j = grp; j < cnt; j += G) {
-            double rec[2 * W];
-#pragma unroll
-            for (int w = 0; w < W; w++) {
-              const double2 u2 = tile[j * W + w];
-              rec[2 * w] = u2.x;
-              rec[2 * w + 1] = u2.y;
-            }
-#pragma unroll
-            for (int t = 0; t < RT; t++) {
-              double r2 = 0.0;
-#pragma unroll
-              for (int k = 0; k < D; k++) {
-                const double dk = x[t][k] - rec[k];
-                r2 = fma(dk, dk, r2);
-              }
-              double kv;
-              if constexpr ((KIND == COULOMB || KIND == LAPLACE) && !SELF) {
-                const double y = rsq_approx(r2);
-                const double e = fma(-r2, y * y, 1.0);
-                kv = fma(y * e, fma(0.375, e, 0.5), y);
-              } else {
-                kv = kpair<KIND>(r2, kp);
-              }
-#pragma unroll
-              for (int r = 0; r < NR; r++) acc[t][r] = fma(kv, rec[D + r], acc[t][r]);
-            }
-          }
-        }
-        __syncthreads();
-      }
+      __syncwarp();
+      stream_members<D, KIND, NR, TILE, SELF, true, RT>(S, rec, 1, o, kp, worker, grp, G, x, acc, ntile);
     }
+    for (int64_t q0 = lb; q0 < le; q0 += MAXMEMW) {
+      const int nmem = (int)(le - q0 < MAXMEMW ? le - q0 : MAXMEMW);
+      member_table<SELF>(T, c, q0, nmem, S);
+      stream_members<D, KIND, NR, TILE, SELF, false, RT>(S, rec, nmem, o, kp, worker, grp, G, x, acc, ntile);
+    }
+    constexpr double SCALE = kscale<KIND>() * (is_inv_r<KIND>() ? 0.5 : 1.0);
 #pragma unroll
     for (int t = 0; t < RT; t++)
 #pragma unroll
-      for (int r = 0; r < NR; r++) part[(t * IT2 + tid) * NR + r] = acc[t][r];
-    __syncthreads();
+      for (int r = 0; r < NR; r++) S.part[(t * 32 + lane) * NR + r] = acc[t][r];
+    __syncwarp();
     if (worker && grp == 0) {
 #pragma unroll
       for (int t = 0; t < RT; t++) {
@@ -229,49 +427,129 @@ __device__ __forceinline__ void interact_cell(const LevelTab& T, int64_t c, int6
 #pragma unroll
         for (int r = 0; r < NR; r++) {
           double tot = 0.0;
-          for (int g = 0; g < G; g++) tot += part[(t * IT2 + g * TS + slot) * NR + r];
-          T.out[(tb + a) * R + r0 + r] = tot * kscale<KIND>();
+          for (int g = 0; g < G; g++) tot += S.part[(t * 32 + g * TS + slot) * NR + r];
+          T.out[(tb + a) * R + r0 + r] = tot * SCALE;
         }
       }
     }
-    __syncthreads();
+    __syncwarp();
   }
 }
 
+// Persistent kernel: every warp pulls work items (descending pair count) from
+// a global counter until the list is exhausted.
 template <int D, int KIND, int NR, int TILE, int RT>
-__global__ void __launch_bounds__(IT2) interact2(const int64_t* __restrict__ items,
-                                                 const LevelTab* __restrict__ tabs, int near_list, int64_t R,
-                                                 int64_t r0, KParams kp) {
-  constexpr int W = SrcW<D, NR>::W;
-  __shared__ double2 tile[W * TILE];
-  __shared__ int64_t pref[MAXMEM + 1];
-  __shared__ int64_t sbeg[MAXMEM];
-  __shared__ int64_t wsum[IT2 / 32];
-  __shared__ double part[2 * IT2 * NR];
-  const int64_t it = items[blockIdx.x];
-  const int lev = (int)(it >> 40);
-  const int64_t c = it & ((1ll << 40) - 1);
-  const LevelTab T = tabs[lev];
-  if (lev == near_list)
-    interact_cell<D, KIND, NR, TILE, true, RT>(T, c, R, r0, kp, tile, pref, sbeg, wsum, part);
-  else
-    interact_cell<D, KIND, NR, TILE, false, RT>(T, c, R, r0, kp, tile, pref, sbeg, wsum, part);
+__global__ void __launch_bounds__(IT2) interact_warps(const int64_t* __restrict__ items, int64_t n_items,
+                                                      unsigned long long* __restrict__ counter,
+                                                      const LevelTab* __restrict__ tabs, int ntabs, int near_list,
+                                                      int64_t R, int64_t r0, KParams kp) {
+  using WS = WarpSmem<D, NR, TILE, RT>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  LevelTab* tab_s = reinterpret_cast<LevelTab*>(smem_raw);
+  const size_t tab_bytes = (sizeof(LevelTab) * ntabs + 127) / 128 * 128;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WS& S = reinterpret_cast<WS*>(smem_raw + tab_bytes)[warp];
+  for (int i = threadIdx.x; i < ntabs; i += blockDim.x) tab_s[i] = tabs[i];
+  if (lane == 0) {
+    mbar_init(&S.bar[0], 1);
+    mbar_init(&S.bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t ntile = 0;
+  for (;;) {
+    unsigned long long idx = 0;
+    if (lane == 0) idx = atomicAdd(counter, 1ull);
+    idx = __shfl_sync(0xffffffffu, idx, 0);
+    if (idx >= (unsigned long long)n_items) break;
+    const int64_t it = items[idx];
+    const int lev = (int)(it >> 40);
+    const int64_t c = it & ((1ll << 40) - 1);
+    const LevelTab& T = tab_s[lev];
+    if (lev == near_list)
+      interact_cell<D, KIND, NR, TILE, true, RT>(T, c, R, r0, kp, S, ntile);
+    else
+      interact_cell<D, KIND, NR, TILE, false, RT>(T, c, R, r0, kp, S, ntile);
+  }
+}
+
+// Records of every source list for one RHS chunk: coordinates (static) and
+// charges of columns [r0, r0 + NR) (per matvec).  One thread per record.
+struct PackTab {
+  const double* sc;  // source coords SoA (ld)
+  int64_t ld;
+  const double* q;   // charges, row stride R
+  double2* rec;      // records
+  int64_t n;         // records in this list
+  int64_t off;       // first global thread of this list
+};
+
+template <int D, int NR>
+__global__ void pack_records(const PackTab* __restrict__ pt, int nlists, int64_t total, int64_t R, int64_t r0,
+                             int coords) {
+  constexpr int W = SrcRec<D, NR>::W;
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= total) return;
+  int l = 0;
+  while (l + 1 < nlists && pt[l + 1].off <= g) l++;
+  const PackTab T = pt[l];
+  const int64_t i = g - T.off;
+  double* r = reinterpret_cast<double*>(T.rec + i * W);
+  if (coords) {
+#pragma unroll
+    for (int k = 0; k < D; k++) r[k] = T.sc[k * T.ld + i];
+#pragma unroll
+    for (int k = D + NR; k < 2 * W; k++) r[k] = 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < NR; q++) r[D + q] = T.q[i * R + r0 + q];
 }
 
 template <int D, int KIND, int NR, int TILE>
 void launch_chunk(const DevH2& h, int64_t R, int64_t r0, const KParams& kp, cudaStream_t s) {
   if (!h.n_items) return;
-  const unsigned g = (unsigned)h.n_items;
   const int nl = h.t->depth + 1;  // list id of the leaf near field
-  auto* items = h.items.get();
+  const int ntabs = nl + 1;
   auto* tabs = reinterpret_cast<const LevelTab*>(h.tabs.get());
-  interact2<D, KIND, NR, TILE, 2><<<g, IT2, 0, s>>>(items, tabs, nl, R, r0, kp);
+  const size_t smem = (sizeof(LevelTab) * ntabs + 127) / 128 * 128 +
+                      (IT2 / 32) * sizeof(WarpSmem<D, NR, TILE, H2B_RT>);
+  auto kern = interact_warps<D, KIND, NR, TILE, H2B_RT>;
+  static int grid = 0;  // per instantiation: persistent grid = resident CTAs
+  static size_t grid_smem = 0;
+  if (grid == 0 || grid_smem != smem) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int dev = 0, nsm = 0, per = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, IT2, smem));
+    grid = nsm * (per > 0 ? per : 1);
+    grid_smem = smem;
+  }
+  // pack this chunk's charges into the records
+  const auto& pk = NR == 1 ? h.pack1 : h.pack16;
+  if (pk.total) {
+    pack_records<D, NR><<<nblk(pk.total, 256), 256, 0, s>>>(reinterpret_cast<const PackTab*>(pk.tabs.get()),
+                                                            pk.nlists, pk.total, R, r0, 0);
+    CKL();
+  }
+  CK(cudaMemsetAsync(h.work_counter.get(), 0, sizeof(unsigned long long), s));
+  const int64_t ng = std::min<int64_t>(grid, (h.n_items + IT2 / 32 - 1) / (IT2 / 32));
+  kern<<<(unsigned)ng, IT2, smem, s>>>(h.items.get(), h.n_items, h.work_counter.get(), tabs, ntabs, nl, R, r0, kp);
+  CKL();
+}
+
+template <int D, int NR>
+void pack_coords_d(const DevH2& h, cudaStream_t s) {
+  const auto& pk = NR == 1 ? h.pack1 : h.pack16;
+  if (pk.total)
+    pack_records<D, NR><<<nblk(pk.total, 256), 256, 0, s>>>(reinterpret_cast<const PackTab*>(pk.tabs.get()),
+                                                            pk.nlists, pk.total, 1, 0, 1);
   CKL();
 }
 
 template <int D, int KIND>
 void launch_interact2(const DevH2& h, int64_t R, int64_t r0, int nr, const KParams& kp, cudaStream_t s) {
-  if (nr == 16) launch_chunk<D, KIND, 16, 64>(h, R, r0, kp, s);
+  if (nr == 16) launch_chunk<D, KIND, 16, H2B_TILE16>(h, R, r0, kp, s);
   else launch_chunk<D, KIND, 1, H2B_TILE1>(h, R, r0, kp, s);
 }
 
@@ -294,5 +572,7 @@ void interact_all_d_impl(int kind, const DevH2& h, int64_t R, int64_t r0, int nr
 
 template <int D>
 void interact_all_d(int kind, const DevH2& h, int64_t R, int64_t r0, int nr, const KParams& kp, cudaStream_t s);
+template <int D>
+void pack_coords_dim(const DevH2& h, int nr, cudaStream_t s);
 
 }  // namespace h2b

@@ -7,4 +7,9 @@ void interact_all_d<2>(int kind, const DevH2& h, int64_t R, int64_t r0, int nr, 
                         cudaStream_t s) {
   interact_all_d_impl<2>(kind, h, R, r0, nr, kp, s);
 }
+template <>
+void pack_coords_dim<2>(const DevH2& h, int nr, cudaStream_t s) {
+  if (nr == 16) pack_coords_d<2, 16>(h, s);
+  else pack_coords_d<2, 1>(h, s);
+}
 }  // namespace h2b

@@ -121,6 +121,15 @@ void interact_all(int d, int kind, const DevH2& h, int64_t R, int64_t r0, int nr
   }
 }
 
+void pack_coords(int d, const DevH2& h, int nr, cudaStream_t s) {
+  switch (d) {
+    case 1: pack_coords_dim<1>(h, nr, s); break;
+    case 2: pack_coords_dim<2>(h, nr, s); break;
+    case 3: pack_coords_dim<3>(h, nr, s); break;
+    default: pack_coords_dim<4>(h, nr, s); break;
+  }
+}
+
 // pair counts per work item (the reference's entry counts for S and near blocks)
 __global__ void item_costs(int64_t n, int lev, const int64_t* __restrict__ t_ptr, const int64_t* __restrict__ s_ptr,
                            const int64_t* __restrict__ l_ptr, const int64_t* __restrict__ l_idx,
@@ -132,7 +141,9 @@ __global__ void item_costs(int64_t n, int lev, const int64_t* __restrict__ t_ptr
     int64_t y = l_idx[q];
     src += s_ptr[y + 1] - s_ptr[y];
   }
-  cost[c] = (unsigned long long)((t_ptr[c + 1] - t_ptr[c]) * src);
+  // +1 keeps cells with targets but no sources (they must write zeros); cells without targets cost 0 and are dropped
+  const int64_t m = t_ptr[c + 1] - t_ptr[c];
+  cost[c] = m > 0 ? (unsigned long long)(m * src) + 1ull : 0ull;
   item[c] = ((int64_t)lev << 40) | c;
 }
 
@@ -184,18 +195,55 @@ void build_items(DevH2& h, cudaStream_t s) {
   tmp.alloc(bytes);
   CK(cub::DeviceRadixSort::SortPairsDescending(tmp.get(), bytes, cost.get(), cost_sorted.get(), item.get(),
                                                h.items.get(), total, 0, 64, s));
-  // drop zero-cost items (cells with no targets or an empty list)
+  // drop zero-cost items (cells without targets)
   auto hc = to_host(cost_sorted.get(), total, s);
   int64_t nz = 0;
   while (nz < total && hc[nz] > 0) nz++;
   h.n_items = nz;
 }
 
-// list tables (target side + output) and source-record packing tables
+// Source records (interact.cuh SrcRec) for RHS width nr: allocation, pack
+// tables and the static coordinate part.
+void build_records(DevH2& h, int nr, cudaStream_t s) {
+  const DevTree& T = *h.t;
+  const int L = T.depth;
+  RecSet& rs = nr == 1 ? h.pack1 : h.pack16;
+  const int rsz = 2 * ((T.d + nr + 1) / 2);  // doubles per record
+  std::vector<PackTab> pt;
+  rs.lists.clear();
+  rs.lists.resize(std::max(L - 1, 0) + 1);
+  int64_t off = 0;
+  auto add = [&](DBuf<double2>& buf, const double* sc, int64_t ld, const double* q, int64_t n) {
+    buf.alloc(std::max<int64_t>(n, 1) * rsz / 2, &h.mem);
+    PackTab t;
+    t.sc = sc;
+    t.ld = ld;
+    t.q = q;
+    t.rec = buf.get();
+    t.n = n;
+    t.off = off;
+    off += n;
+    pt.push_back(t);
+  };
+  for (int l = 2; l <= L; l++) {
+    const DevH2Level& HL = h.lv[l];
+    add(rs.lists[l - 2], HL.sout_cd(), std::max<int64_t>(HL.out_total, 1), h.wout[l].get(), HL.out_total);
+  }
+  add(rs.lists[std::max(L - 1, 0)], T.ssd(), T.nq, h.w_sorted.get(), T.nq);
+  rs.nlists = (int)pt.size();
+  rs.total = off;
+  rs.tabs.alloc(sizeof(PackTab) * pt.size(), &h.mem);
+  CK(cudaMemcpyAsync(rs.tabs.get(), pt.data(), sizeof(PackTab) * pt.size(), cudaMemcpyHostToDevice, s));
+  pack_coords(T.d, h, nr, s);
+  CK(cudaStreamSynchronize(s));
+}
+
+// list tables (target side + output) for the interaction kernel
 void build_tabs(DevH2& h, int64_t R, cudaStream_t s) {
   const DevTree& T = *h.t;
   const int L = T.depth;
   std::vector<LevelTab> tabs(L + 2);
+  auto rec = [&](const RecSet& rs, int i) -> const double2* { return rs.lists.empty() ? nullptr : rs.lists[i].get(); };
   for (int l = 0; l <= L + 1; l++) {
     LevelTab& t = tabs[l];
     std::memset(&t, 0, sizeof t);
@@ -205,10 +253,9 @@ void build_tabs(DevH2& h, int64_t R, cudaStream_t s) {
       t.tc = HL.tin_c.get();
       t.ld_t = std::max<int64_t>(HL.in_total, 1);
       t.t_ptr = HL.in_ptr.get();
-      t.sc = HL.sout_cd();
-      t.ld_s = std::max<int64_t>(HL.out_total, 1);
       t.s_ptr = HL.out_ptrd();
-      t.q = h.wout[l].get();
+      t.rec1 = rec(h.pack1, l - 2);
+      t.rec16 = rec(h.pack16, l - 2);
       t.l_ptr = Lv.il_ptr.get();
       t.l_idx = Lv.il_idx.get();
       t.out = h.uin[l].get();
@@ -217,10 +264,9 @@ void build_tabs(DevH2& h, int64_t R, cudaStream_t s) {
       t.tc = T.tsd();
       t.ld_t = T.np;
       t.t_ptr = Lv.t_ptr.get();
-      t.sc = T.ssd();
-      t.ld_s = T.nq;
       t.s_ptr = T.shared ? Lv.t_ptr.get() : Lv.s_ptr.get();
-      t.q = h.w_sorted.get();
+      t.rec1 = rec(h.pack1, std::max(L - 1, 0));
+      t.rec16 = rec(h.pack16, std::max(L - 1, 0));
       t.l_ptr = Lv.nb_ptr.get();
       t.l_idx = Lv.nb_idx.get();
       t.out = h.near.get();
@@ -245,6 +291,7 @@ void ensure_scratch(DevH2& h, int64_t R, cudaStream_t s) {
     h.uin[l].alloc(std::max<int64_t>(h.lv[l].in_total * R, 1), &h.mem);
   }
   if (!h.items.n) build_items(h, s);
+  if (!h.work_counter.n) h.work_counter.alloc(1, &h.mem);
   if (h.own_in.empty()) {
     h.own_in.resize(T.depth + 1);
     h.own_out.resize(T.depth + 1);
@@ -274,6 +321,10 @@ void ensure_scratch(DevH2& h, int64_t R, cudaStream_t s) {
     fill_owner<<<nblk(Lf.n, 256), 256, 0, s>>>(Lf.n, Lf.t_ptr.get(), h.own_t.get());
     CKL();
   }
+  h.pack1 = RecSet();
+  h.pack16 = RecSet();
+  if (R >= 16) build_records(h, 16, s);
+  if (R % 16) build_records(h, 1, s);
   build_tabs(h, R, s);
   h.scratch_nrhs = R;
 }
@@ -304,9 +355,9 @@ int64_t matvec_launches(const DevH2& h, int64_t nrhs) {
   std::vector<std::pair<int64_t, int>> ch;
   rhs_chunks(nrhs, ch);
   int64_t nchunk = (int64_t)ch.size();
-  if (L < 2) return 1 + nchunk + 1;
-  // gather, P2M, M2M x (L-2), interaction x chunks, L2L x (L-2), L2P+scatter
-  return 1 + 1 + (L - 2) + nchunk + (L - 2) + 1;
+  // gather, P2M, M2M x (L-2), (record pack + interaction) x chunks, L2L x (L-2), L2P+scatter
+  if (L < 2) return 1 + 2 * nchunk + 1;
+  return 1 + 1 + (L - 2) + 2 * nchunk + (L - 2) + 1;
 }
 
 void matvec(DevH2& h, const double* w, double* u, int64_t R, cudaStream_t s) {

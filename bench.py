@@ -45,7 +45,13 @@ CONFIGS = {
     "c4": ("uniform", 4194304, 2, 4, "coulomb-3d", {}, 128, 1e-10, "normal", 16),
 }
 HEADLINE = "c2"
-FLOPS_PER_PAIR = 18  # 1/r entry: 3 DADD + (DMUL + 2 DFMA) r^2 + (2 DMUL + 3 DFMA) rsqrt correction + DFMA accumulate
+# FP64 flops the interaction kernel executes per 1/r pair (DFMA = 2, DADD / DMUL = 1; MUFU.RSQ64H seed not
+# counted), one RHS; each further RHS adds one DFMA (2 flops):
+#   M2L (interact.cuh pair_r2 + acc_inv_r): r^2 = DADD + 3 DFMA (7); cubic rsqrt step DMUL + 3 DFMA (7);
+#        charge DMUL + accumulate DFMA (3)                                                        -> 17
+#   near field: r^2 = 3 DADD + 3 DFMA (9); quadratic step DMUL + DFMA (3); DMUL + DFMA (3)       -> 15
+FLOPS_PER_PAIR_M2L = 17
+FLOPS_PER_PAIR_NEAR = 15
 
 
 def make_inputs(cfg, n_override=None):
@@ -293,8 +299,7 @@ def run_b200(args, cfg, world, rank, local):
     stage = stage_times(h2, wd, repeats=max(3, min(args.steps, 10)))  # [up, m2l, l2l, near+l2p, total]
     peak = ctypes_peak(L)
     inter_ms = stage[1] + stage[3]
-    flops = FLOPS_PER_PAIR * nrhs * (pairs_m2l + pairs_p2p) if nrhs == 1 else \
-        (pairs_m2l + pairs_p2p) * (FLOPS_PER_PAIR - 2 + 2 * nrhs)
+    flops = pairs_m2l * (FLOPS_PER_PAIR_M2L + 2 * (nrhs - 1)) + pairs_p2p * (FLOPS_PER_PAIR_NEAR + 2 * (nrhs - 1))
     achieved = flops / (inter_ms * 1e-3) / 1e12
     traffic = load_traffic()
 
@@ -322,7 +327,8 @@ def run_b200(args, cfg, world, rank, local):
         "gpu_launches": int(matvec_launches(h2, nrhs)) * args.steps,
         "roofline": {"bound": "fp64", "kernel": "interact_kernel (M2L all levels + near field/L2P)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                     "traffic": traffic, "flops_per_pair": FLOPS_PER_PAIR,
+                     "traffic": traffic,
+                     "flops_per_pair": {"m2l": FLOPS_PER_PAIR_M2L, "near": FLOPS_PER_PAIR_NEAR},
                      "peak_source": "measured: DFMA throughput probe (h2b_fp64_peak) on this GPU, same run"},
         "clocks": clk.summary(),
     }

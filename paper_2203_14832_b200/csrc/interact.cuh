@@ -67,6 +67,12 @@ namespace {
 #ifndef H2B_RT
 #define H2B_RT 2
 #endif
+#ifndef H2B_UNROLL
+#define H2B_UNROLL 2
+#endif
+#ifndef H2B_MINB
+#define H2B_MINB 1
+#endif
 #ifndef H2B_TILE16
 #define H2B_TILE16 32
 #endif
@@ -77,7 +83,8 @@ constexpr int IT2 = H2B_IT2;
 #ifndef H2B_MAXMEMW
 #define H2B_MAXMEMW 256
 #endif
-constexpr int MAXMEMW = H2B_MAXMEMW;  // list members per member table
+constexpr int MAXMEMW = H2B_MAXMEMW;
+constexpr int UNROLL_J = H2B_UNROLL;  // source-loop unroll (independent pair chains per lane)
 
 // doubles per source record (padded to whole 16-byte words for TMA / LDS.128)
 template <int D, int NR>
@@ -220,14 +227,14 @@ struct WarpSmem {
   double yy[TILE];             // |y'|^2 of the current tile (interaction lists)
   uint64_t bar[2];             // "tile landed" mbarriers
   int pref[MAXMEMW + 1];       // prefix of member lengths (records)
-  int64_t sbeg[MAXMEMW];       // first record of each member
+  int sbeg[MAXMEMW];           // first record of each member (records < 2^31, checked on the host)
   double part[RT * 32 * NR];   // per-group partial sums
 };
 
 // Issue the TMA bulk copies of window [p0, p0 + cnt) of the member
 // concatenation into one stage (whole warp; lane 0 arms the mbarrier first).
 template <int W>
-__device__ __forceinline__ void issue_tile(const double2* rec, int nmem, const int* pref, const int64_t* sbeg,
+__device__ __forceinline__ void issue_tile(const double2* rec, int nmem, const int* pref, const int* sbeg,
                                            int p0, int cnt, double2* dst, uint64_t* bar) {
   const int lane = threadIdx.x & 31;
   if (lane == 0) mbar_expect_tx(bar, (uint32_t)cnt * (uint32_t)(W * 16));
@@ -243,7 +250,7 @@ __device__ __forceinline__ void issue_tile(const double2* rec, int nmem, const i
     const int pa = pref[qm] > p0 ? pref[qm] : p0;
     const int pb = pref[qm + 1] < p1 ? pref[qm + 1] : p1;
     if (pb > pa)
-      bulk_g2s(dst + (pa - p0) * W, rec + (sbeg[qm] + (pa - pref[qm])) * W, (uint32_t)(pb - pa) * (W * 16), bar);
+      bulk_g2s(dst + (pa - p0) * W, rec + (int64_t)(sbeg[qm] + (pa - pref[qm])) * W, (uint32_t)(pb - pa) * (W * 16), bar);
   }
 }
 
@@ -297,7 +304,7 @@ __device__ __forceinline__ void stream_members(WarpSmem<D, NR, TILE, RT>& S, con
                     &S.bar[b ^ 1]);
     }
     if (worker) {
-#pragma unroll 2
+#pragma unroll (UNROLL_J)
       for (int j = grp; j < cnt; j += G) {
         double v[2 * W];
 #pragma unroll
@@ -337,7 +344,7 @@ __device__ __forceinline__ void member_table(const LevelTab& T, int64_t c, int64
     if (q < nmem) {
       const int64_t sc = T.l_idx[q0 + q];
       const int64_t sb = T.s_ptr[sc];
-      S.sbeg[q] = sb;
+      S.sbeg[q] = (int)sb;
       len = (SELF && sc == c) ? 0 : (int)(T.s_ptr[sc + 1] - sb);
     }
     int v = len;
@@ -401,7 +408,7 @@ __device__ __forceinline__ void interact_cell(const LevelTab& T, int64_t c, int6
     if constexpr (SELF) {  // own leaf: the only member that can hold r2 == 0
       if (lane == 0) {
         const int64_t b = T.s_ptr[c];
-        S.sbeg[0] = b;
+        S.sbeg[0] = (int)b;
         S.pref[0] = 0;
         S.pref[1] = (int)(T.s_ptr[c + 1] - b);
       }
@@ -439,7 +446,7 @@ __device__ __forceinline__ void interact_cell(const LevelTab& T, int64_t c, int6
 // Persistent kernel: every warp pulls work items (descending pair count) from
 // a global counter until the list is exhausted.
 template <int D, int KIND, int NR, int TILE, int RT>
-__global__ void __launch_bounds__(IT2) interact_warps(const int64_t* __restrict__ items, int64_t n_items,
+__global__ void __launch_bounds__(IT2, H2B_MINB) interact_warps(const int64_t* __restrict__ items, int64_t n_items,
                                                       unsigned long long* __restrict__ counter,
                                                       const LevelTab* __restrict__ tabs, int ntabs, int near_list,
                                                       int64_t R, int64_t r0, KParams kp) {

@@ -230,6 +230,7 @@ void build_records(DevH2& h, int nr, cudaStream_t s) {
     add(rs.lists[l - 2], HL.sout_cd(), std::max<int64_t>(HL.out_total, 1), h.wout[l].get(), HL.out_total);
   }
   add(rs.lists[std::max(L - 1, 0)], T.ssd(), T.nq, h.w_sorted.get(), T.nq);
+  if (off >= ((int64_t)1 << 31)) throw std::invalid_argument("more than 2^31 source records");
   rs.nlists = (int)pt.size();
   rs.total = off;
   rs.tabs.alloc(sizeof(PackTab) * pt.size(), &h.mem);

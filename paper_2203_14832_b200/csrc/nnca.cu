@@ -16,6 +16,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
@@ -26,7 +27,7 @@ namespace h2b {
 
 namespace {
 
-constexpr int ACA_MAX_THREADS = 256;
+constexpr int ACA_MAX_THREADS = 1024;
 constexpr int ACA_MAX_WARPS = ACA_MAX_THREADS / 32;
 constexpr int XCH = 8;  // cross-product partial sums per pass
 
@@ -59,53 +60,73 @@ struct RedScratch {
   double v[ACA_MAX_WARPS];
   long long i[ACA_MAX_WARPS];
   double x[ACA_MAX_WARPS][XCH];
+  double bv;     // block result (value)
+  long long bi;  // block result (index)
 };
 
+// Block reductions: warp shuffles, then warp 0 reduces the per-warp results
+// and broadcasts through shared memory (two barriers).
 template <int NT>
 __device__ void block_argmax(double& v, int64_t& i, RedScratch& rs) {
-  constexpr int ACA_WARPS = NT / 32;
-  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   warp_argmax(v, i);
-  __syncthreads();
   if (lane == 0) {
     rs.v[w] = v;
     rs.i[w] = i;
   }
   __syncthreads();
-  v = -1.0;
-  i = -1;
-  for (int q = 0; q < ACA_WARPS; q++) argmax_merge(v, i, rs.v[q], rs.i[q]);
+  if (w == 0) {
+    double v2 = lane < NW ? rs.v[lane] : -1.0;
+    int64_t i2 = lane < NW ? (int64_t)rs.i[lane] : -1;
+    warp_argmax(v2, i2);
+    if (lane == 0) {
+      rs.bv = v2;
+      rs.bi = i2;
+    }
+  }
+  __syncthreads();
+  v = rs.bv;
+  i = rs.bi;
 }
 
 template <int NT>
 __device__ double block_sum(double x, RedScratch& rs) {
-  constexpr int ACA_WARPS = NT / 32;
-  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   x = warp_sum(x);
-  __syncthreads();
   if (lane == 0) rs.v[w] = x;
   __syncthreads();
-  double s = 0.0;
-  for (int q = 0; q < ACA_WARPS; q++) s += rs.v[q];
-  return s;
+  if (w == 0) {
+    // fixed left-to-right order over warps (deterministic)
+    double s2 = 0.0;
+    if (lane == 0)
+      for (int q = 0; q < NW; q++) s2 += rs.v[q];
+    if (lane == 0) rs.bv = s2;
+  }
+  __syncthreads();
+  return rs.bv;
 }
 
 template <int NT>
 __device__ int64_t block_min(int64_t x, RedScratch& rs) {
-  constexpr int ACA_WARPS = NT / 32;
-  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   x = warp_min_i64(x);
-  __syncthreads();
   if (lane == 0) rs.i[w] = x;
   __syncthreads();
-  int64_t s = INT64_MAX;
-  for (int q = 0; q < ACA_WARPS; q++) s = rs.i[q] < s ? rs.i[q] : s;
-  return s;
+  if (w == 0) {
+    int64_t y = lane < NW ? (int64_t)rs.i[lane] : INT64_MAX;
+    y = warp_min_i64(y);
+    if (lane == 0) rs.bi = y;
+  }
+  __syncthreads();
+  return rs.bi;
 }
 
 // _core.pyx:184-305, one CTA per cell
 template <int D, int NT>
-__global__ void __launch_bounds__(NT, 2048 / NT / 2) aca_kernel(AcaArgs A) {
+__global__ void __launch_bounds__(NT, (2048 / NT / 2) > 0 ? (2048 / NT / 2) : 1) aca_kernel(AcaArgs A) {
   constexpr int ACA_THREADS = NT;
   constexpr int ACA_WARPS = NT / 32;
   extern __shared__ double sm[];
@@ -478,6 +499,440 @@ size_t workspace_budget() {
   return std::max<size_t>(b, (size_t)256 << 20);
 }
 
+// ---------------------------------------------------------------------
+// Persistent level-batched ACA (the setup hot path).
+//
+// One CTA per SM (NT = 512 or 1024 threads) pulls cells from a work queue
+// (largest first).  Its workspace (residual factors U, V, the gathered far
+// candidates, used-row/column flags) is a fixed per-CTA slab reused cell
+// after cell, so the working set of all resident cells (~148 x k x n x 8 B)
+// stays in the 126 MB L2: the ACA re-reads V (k x n) at every step, which in
+// a one-CTA-per-cell launch (thousands of cells resident) went to DRAM.
+// The far candidates of a cell are gathered from its interaction list into
+// the slab once, and the interpolation operator (aca.py:476 / :490) is
+// formed right after the ACA from the same slab.  Pivot arithmetic is
+// unchanged (reference operation order, see aca_kernel).
+// ---------------------------------------------------------------------
+#ifdef H2B_ACA_PROF
+__device__ unsigned long long g_aca_prof[8];
+#define APROF(i)                                                    \
+  do {                                                              \
+    __syncthreads();                                                \
+    if (tid == 0) {                                                 \
+      const long long now_ = clock64();                             \
+      atomicAdd(&g_aca_prof[i], (unsigned long long)(now_ - last_)); \
+      last_ = now_;                                                 \
+    }                                                               \
+  } while (0)
+#else
+#define APROF(i) \
+  do {           \
+  } while (0)
+#endif
+
+struct CellJob {
+  int kind;
+  double a, eps2;
+  int64_t ncell;
+  const int64_t* order;  // cells, largest first
+  int rows_far;          // rows = far candidates (outgoing side) instead of own points
+  Src own, far;
+  const int64_t* il_ptr;
+  const int64_t* il_idx;
+  const int64_t* caps;
+  const int64_t* piv_off;
+  int64_t *tpiv, *spiv, *rank, *conv, *nevals;
+  double* mat;
+  const int64_t* mat_off;
+  int which;  // 0: row interpolator from U (rows m); 1: column interpolator from V (rows n)
+  double* ws;
+  int64_t ws_doubles;  // per CTA
+  int64_t m_max, n_max, f_max, cap_max;
+  unsigned long long* counter;
+};
+
+#ifndef H2B_ACA_MINB
+#define H2B_ACA_MINB 1
+#endif
+template <int D, int NT, int CPT, bool VSMEM, bool USMEM>
+__global__ void __launch_bounds__(NT, VSMEM ? 1 : H2B_ACA_MINB) aca_cells(CellJob J) {
+  constexpr int NW = NT / 32;
+  extern __shared__ double sm[];
+  __shared__ RedScratch rs;
+  __shared__ double xt[D], yb[D];
+  __shared__ long long s_cell;
+  __shared__ int64_t s_mp[NT + 1];   // member prefix (far gather)
+  __shared__ int64_t s_mb[NT];       // member range begin
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* urow = sm;
+  double* vcol = sm + J.cap_max;
+  double* crossv = sm + 2 * J.cap_max;
+  double* crossu = sm + 3 * J.cap_max;
+  double* base = J.ws + (int64_t)blockIdx.x * J.ws_doubles;
+  double* Ub = base;
+  double* Vb = Ub + J.cap_max * J.m_max;
+  double* FC = Vb + J.cap_max * J.n_max;
+  int64_t* FG = reinterpret_cast<int64_t*>(FC + D * J.f_max);
+  int64_t* RP = FG + J.f_max;
+  int64_t* CP = RP + J.cap_max;
+  unsigned char* flags = reinterpret_cast<unsigned char*>(CP + J.cap_max);
+  long long last_ = clock64();
+  (void)last_;
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) {
+      const unsigned long long q = atomicAdd(J.counter, 1ull);
+      s_cell = q < (unsigned long long)J.ncell ? (long long)J.order[q] : -1ll;
+    }
+    __syncthreads();
+    const int64_t cell = s_cell;
+    if (cell < 0) break;
+    // ---- own range and far candidates (gathered into the slab) ----
+    int64_t ob, oe;
+    src_range(J.own, cell, ob, oe);
+    const int64_t own_n = oe - ob;
+    const int64_t lb = J.il_ptr[cell], le = J.il_ptr[cell + 1];
+    int64_t far_n = 0;
+    for (int64_t q0 = lb; q0 < le; q0 += NT) {
+      const int nm = (int)(le - q0 < NT ? le - q0 : NT);
+      int64_t len = 0;
+      if (tid < nm) {
+        int64_t b, e;
+        src_range(J.far, J.il_idx[q0 + tid], b, e);
+        s_mb[tid] = b;
+        len = e - b;
+      }
+      int64_t v = len;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long n2 = __shfl_up_sync(0xffffffffu, (long long)v, o);
+        if (lane >= o) v += n2;
+      }
+      if (lane == 31) rs.i[warp] = v;
+      __syncthreads();
+      int64_t off = far_n;
+      for (int w = 0; w < warp; w++) off += rs.i[w];
+      if (tid < nm) s_mp[tid + 1] = off + v;
+      if (tid == 0) s_mp[0] = far_n;
+      int64_t tot = far_n;
+      for (int w = 0; w < NW; w++) tot += rs.i[w];
+      __syncthreads();
+      for (int q = warp; q < nm; q += NW) {
+        const int64_t b = s_mb[q], o0 = s_mp[q], len2 = s_mp[q + 1] - o0;
+        for (int64_t e = lane; e < len2; e += 32) {
+#pragma unroll
+          for (int k = 0; k < D; k++) FC[k * J.f_max + o0 + e] = J.far.coords[k * J.far.ld + b + e];
+          FG[o0 + e] = J.far.gidx[b + e];
+        }
+      }
+      far_n = tot;
+      __syncthreads();
+    }
+    APROF(0);
+    const int64_t m = J.rows_far ? far_n : own_n;
+    const int64_t n = J.rows_far ? own_n : far_n;
+    const int64_t cap = J.caps[cell];
+    // row / column coordinate k of local index i
+    auto rowc = [&](int k, int64_t i) -> double {
+      return J.rows_far ? FC[k * J.f_max + i] : J.own.coords[k * J.own.ld + ob + i];
+    };
+    auto colc = [&](int k, int64_t j) -> double {
+      return J.rows_far ? J.own.coords[k * J.own.ld + ob + j] : FC[k * J.f_max + j];
+    };
+    if (m == 0 || n == 0 || cap == 0) {
+      if (tid == 0) {
+        J.rank[cell] = 0;
+        J.conv[cell] = (m == 0 || n == 0) ? 1 : 0;
+        J.nevals[cell] = 0;
+      }
+      continue;
+    }
+    // shared-memory residents after the 4 cap-sized vectors: U (cap x m) if USMEM, then V (cap x n) if VSMEM
+    double* U = USMEM ? sm + 4 * J.cap_max : Ub;
+    double* V = VSMEM ? sm + 4 * J.cap_max + (USMEM ? cap * m : 0) : Vb;
+    unsigned char* ru = flags;
+    unsigned char* cu = flags + m;
+    for (int64_t q = tid; q < m + n; q += NT) ru[q] = 0;
+    const int64_t full = m < n ? m : n;
+    int64_t k = 0, trial = 0, nev = 0;
+    double norm2 = 0.0;
+    int64_t converged = 1;
+    __syncthreads();
+    // Step k's row pass also finishes step k - 1 (fused, one sweep over V):
+    // it normalises the raw residual row k - 1 (V[k-1] /= piv, written back),
+    // forms crossv[t] = <V[t], V[k-1]> and |V[k-1]|^2, and only then is step
+    // k - 1's stopping test evaluated -- the row pass of step k is
+    // speculative and discarded (with its evaluation count) if step k - 1
+    // stops.  Pivots, residual arithmetic and the test are unchanged; only the
+    // summation order of the norm bookkeeping differs from the reference.
+    double* crosspart = sm + 4 * J.cap_max + (USMEM ? cap * m : 0) + (VSMEM ? cap * n : 0);  // [NW][cap]
+    bool pend = false;          // step k - 1 awaits normalisation + stopping test
+    double piv_prev = 1.0, u2_prev = 0.0;
+    const int ni = (int)n;
+    // normalise row r = k - 1 on its own (and optionally its cross products): used when no fused pass follows
+    auto finish_row = [&](int r, bool need_cross) -> double {
+      double v2p = 0.0;
+      double* Vr = V + (int64_t)r * n;
+      for (int j = tid; j < ni; j += NT) {
+        const double v = __ddiv_rn(Vr[j], piv_prev);
+        Vr[j] = v;
+        v2p += v * v;
+      }
+      __syncthreads();
+      if (need_cross) {
+        for (int t = warp; t < r; t += NW) {
+          const double* Vt = V + (int64_t)t * n;
+          double s0 = 0.0, s1 = 0.0;
+          int j = lane;
+          for (; j + 32 < ni; j += 64) {
+            s0 = fma(Vt[j], Vr[j], s0);
+            s1 = fma(Vt[j + 32], Vr[j + 32], s1);
+          }
+          for (; j < ni; j += 32) s0 = fma(Vt[j], Vr[j], s0);
+          const double w = warp_sum(s0 + s1);
+          if (lane == 0) crossv[t] = w;
+        }
+      }
+      return block_sum<NT>(v2p, rs);  // syncs: crossv visible
+    };
+    for (;;) {
+      bool exhausted = false, stop_prev = false, fuse = pend;
+      double best;
+      int64_t bj;
+      for (;;) {
+        if (tid == 0) ru[trial] = 1;
+        for (int64_t t = tid; t < k; t += NT) urow[t] = U[t * m + trial];
+        if (tid < D) xt[tid] = rowc(tid, trial);
+        if (fuse)
+          for (int q = tid; q < NW * (int)cap; q += NT) crosspart[q] = 0.0;
+        __syncthreads();
+        double xl[D];
+#pragma unroll
+        for (int q = 0; q < D; q++) xl[q] = xt[q];
+        best = -1.0;
+        bj = -1;
+        const int ki = (int)k;
+        const int kf = fuse ? ki - 1 : ki;  // rows read as already normalised
+        double v2p = 0.0;
+        double* Vlast = V + (int64_t)(ki - 1) * n;
+        // warp-uniform trip count (the fused pass reduces across lanes); columns past n are masked
+        for (int jb = 0; jb < ni; jb += CPT * NT) {
+          const int j0 = jb + tid;
+          double acc[CPT], vl[CPT];
+          int jc[CPT];
+#pragma unroll
+          for (int c = 0; c < CPT; c++) {
+            const int jj = j0 + c * NT;
+            jc[c] = jj < ni ? jj : 0;
+            double y[D];
+#pragma unroll
+            for (int q = 0; q < D; q++) y[q] = colc(q, jc[c]);
+            acc[c] = kval_exact(J.kind, J.a, r2_exact<D>(xl, y));
+            vl[c] = 0.0;
+            if (fuse && jj < ni) {  // normalise row k - 1 in passing
+              vl[c] = __ddiv_rn(Vlast[jj], piv_prev);
+              Vlast[jj] = vl[c];
+              v2p += vl[c] * vl[c];
+            }
+          }
+          const double* Vt = V;
+          if (fuse) {
+            for (int t0 = 0; t0 < kf; t0 += 4, Vt += 4 * (int64_t)n) {
+              double p[4];
+#pragma unroll
+              for (int tt = 0; tt < 4; tt++) {
+                p[tt] = 0.0;
+                if (t0 + tt < kf) {
+                  const double ut = urow[t0 + tt];
+                  const double* Vr = Vt + (int64_t)tt * n;
+#pragma unroll
+                  for (int c = 0; c < CPT; c++) {
+                    const double v = Vr[jc[c]];
+                    acc[c] = __dsub_rn(acc[c], __dmul_rn(ut, v));
+                    p[tt] = fma(v, vl[c], p[tt]);
+                  }
+                }
+              }
+              // transpose-reduce 4 partial sums over the warp: lane gets t = t0 + ((lane >> 3) & 3)
+              const bool b4 = lane & 16, b3 = lane & 8;
+              double k0 = b4 ? p[2] : p[0], k1 = b4 ? p[3] : p[1];
+              k0 += __shfl_xor_sync(0xffffffffu, b4 ? p[0] : p[2], 16);
+              k1 += __shfl_xor_sync(0xffffffffu, b4 ? p[1] : p[3], 16);
+              double kk = b3 ? k1 : k0;
+              kk += __shfl_xor_sync(0xffffffffu, b3 ? k0 : k1, 8);
+              kk += __shfl_xor_sync(0xffffffffu, kk, 4);
+              kk += __shfl_xor_sync(0xffffffffu, kk, 2);
+              kk += __shfl_xor_sync(0xffffffffu, kk, 1);
+              const int tq = t0 + ((lane >> 3) & 3);
+              if ((lane & 7) == 0 && tq < kf) crosspart[warp * cap + tq] += kk;
+            }
+#pragma unroll
+            for (int c = 0; c < CPT; c++) acc[c] = __dsub_rn(acc[c], __dmul_rn(urow[ki - 1], vl[c]));
+          } else {
+#pragma unroll 4
+            for (int t = 0; t < ki; t++, Vt += ni) {
+              const double ut = urow[t];
+#pragma unroll
+              for (int c = 0; c < CPT; c++) acc[c] = __dsub_rn(acc[c], __dmul_rn(ut, Vt[jc[c]]));
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < CPT; c++) {
+            const int jj = j0 + c * NT;
+            if (jj < ni) {
+              V[(int64_t)k * n + jj] = acc[c];
+              if (!cu[jj]) {
+                const double val = fabs(acc[c]);
+                if (val > best) {
+                  best = val;
+                  bj = jj;
+                }
+              }
+            }
+          }
+        }
+        APROF(1);
+        if (bj < 0) best = -1.0;
+        block_argmax<NT>(best, bj, rs);
+        APROF(2);
+        if (fuse) {  // finish step k - 1: cross products, norm update, stopping test
+          for (int t = tid; t < kf; t += NT) {
+            double w = 0.0;
+            for (int q = 0; q < NW; q++) w += crosspart[q * cap + t];
+            crossv[t] = w;
+          }
+          const double v2 = block_sum<NT>(v2p, rs);  // syncs: crossv visible
+          for (int t = 0; t < kf; t++) norm2 += 2.0 * crossu[t] * crossv[t];
+          norm2 += u2_prev * v2;
+          pend = false;
+          fuse = false;
+          if (u2_prev * v2 <= J.eps2 * (norm2 > 0.0 ? norm2 : 0.0)) {
+            stop_prev = true;
+            break;
+          }
+        }
+        nev += n;
+        if (best > 0.0) break;
+        int64_t first = INT64_MAX;
+        for (int64_t i = tid; i < m; i += NT)
+          if (!ru[i] && i < first) first = i;
+        first = block_min<NT>(first, rs);
+        if (first == INT64_MAX) {
+          exhausted = true;
+          break;
+        }
+        trial = first;
+        __syncthreads();
+      }
+      if (stop_prev || exhausted) break;
+      // pivot of step k; the row stays raw until the next pass normalises it
+      const double piv = V[k * n + bj];
+      if (tid < D) yb[tid] = colc(tid, bj);
+      for (int64_t t = tid; t < k; t += NT) vcol[t] = V[t * n + bj];
+      __syncthreads();
+      if (tid == 0) cu[bj] = 1;
+      APROF(3);
+      double yl[D];
+#pragma unroll
+      for (int q = 0; q < D; q++) yl[q] = yb[q];
+      double u2p = 0.0;
+      for (int64_t i = tid; i < m; i += NT) {
+        double xl[D];
+#pragma unroll
+        for (int q = 0; q < D; q++) xl[q] = rowc(q, i);
+        double acc = kval_exact(J.kind, J.a, r2_exact<D>(xl, yl));
+        for (int64_t t = 0; t < k; t++) acc = __dsub_rn(acc, __dmul_rn(U[t * m + i], vcol[t]));
+        U[k * m + i] = acc;
+        u2p += acc * acc;
+      }
+      nev += m;
+      __syncthreads();
+      for (int64_t t = warp; t < k; t += NW) {
+        double sacc = 0.0;
+        const double* Ut = U + t * m;
+        const double* Uk = U + k * m;
+        for (int64_t i = lane; i < m; i += 32) sacc += Ut[i] * Uk[i];
+        sacc = warp_sum(sacc);
+        if (lane == 0) crossu[t] = sacc;
+      }
+      APROF(5);
+      const double u2 = block_sum<NT>(u2p, rs);  // syncs: crossu visible
+      if (tid == 0) {
+        RP[k] = trial;
+        CP[k] = bj;
+      }
+      piv_prev = piv;
+      u2_prev = u2;
+      k += 1;
+      if (k == full) {  // the reference stops here whatever its eps test says (converged stays true)
+        finish_row((int)k - 1, false);
+        break;
+      }
+      if (k == cap) {  // eps test decides between converged and not
+        const double v2 = finish_row((int)k - 1, true);
+        for (int64_t t = 0; t < k - 1; t++) norm2 += 2.0 * crossu[t] * crossv[t];
+        norm2 += u2 * v2;
+        if (!(u2 * v2 <= J.eps2 * (norm2 > 0.0 ? norm2 : 0.0))) converged = 0;
+        break;
+      }
+      best = -1.0;
+      int64_t bi = -1;
+      const double* Uk = U + (k - 1) * m;
+      for (int64_t i = tid; i < m; i += NT)
+        if (!ru[i]) {
+          const double val = fabs(Uk[i]);
+          if (val > best) {
+            best = val;
+            bi = i;
+          }
+        }
+      block_argmax<NT>(best, bi, rs);
+      APROF(6);
+      if (bi < 0) {  // the reference breaks after its (here irrelevant) stopping test
+        finish_row((int)k - 1, false);
+        break;
+      }
+      trial = bi;
+      pend = true;
+      __syncthreads();
+    }
+    __syncthreads();
+    APROF(6);
+    const int64_t po = J.piv_off[cell];
+    if (tid == 0) {
+      J.rank[cell] = k;
+      J.conv[cell] = converged;
+      J.nevals[cell] = nev;
+    }
+    for (int64_t t = tid; t < k; t += NT) {
+      const int64_t r = RP[t], c = CP[t];
+      J.tpiv[po + t] = J.rows_far ? FG[r] : J.own.gidx[ob + r];
+      J.spiv[po + t] = J.rows_far ? J.own.gidx[ob + c] : FG[c];
+    }
+    // interpolation operator (interp_kernel, same arithmetic): which 0 -> P = U L^{-1}; 1 -> Q = V R^{-T}
+    if (k > 0) {
+      const int64_t rows = J.which == 0 ? m : n;
+      const double* F = J.which == 0 ? U : V;
+      const int64_t* pv = J.which == 0 ? RP : CP;
+      double* P = J.mat + J.mat_off[cell];
+      for (int64_t i = tid; i < rows; i += NT) {
+        for (int64_t sI = k - 1; sI >= 0; sI--) {
+          const double* Fs = F + sI * rows;
+          double acc = Fs[i];
+          for (int64_t t = sI + 1; t < k; t++) acc -= P[t * rows + i] * Fs[pv[t]];
+          P[sI * rows + i] = J.which == 0 ? acc / Fs[pv[sI]] : acc;
+        }
+      }
+      __syncthreads();
+      for (int64_t q = tid; q < k * k; q += NT) {
+        const int64_t t = q / k, sI = q % k;
+        P[sI * rows + pv[t]] = (sI == t) ? 1.0 : 0.0;
+      }
+    }
+    APROF(7);
+  }
+}
+
 template <int D, int NT>
 void set_aca_smem(size_t bytes) {
   static size_t done = 0;
@@ -497,28 +952,47 @@ struct SideResult {
   DBuf<int64_t> mat_off, mat_rows;
 };
 
+#ifndef H2B_ACA_NT
+#define H2B_ACA_NT 1024
+#endif
+#ifndef H2B_ACA_CPT
+#define H2B_ACA_CPT 4
+#endif
+#ifndef H2B_ACA_NT_S
+#define H2B_ACA_NT_S 512
+#endif
+#ifndef H2B_ACA_VSMEM_KB
+#define H2B_ACA_VSMEM_KB 200
+#endif
+
 template <int D>
 void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const Src& far, int kind, double a,
               double eps, int64_t max_rank, int which_interp, SideResult& R, cudaStream_t s) {
+  constexpr int NT = H2B_ACA_NT, CPT = H2B_ACA_CPT;
   const DevLevel& L = T.lv[level];
   const int64_t n = L.n;
   DBuf<int64_t> own_b, own_len, far_len;
-  own_b.alloc(n);
-  own_len.alloc(n);
-  far_len.alloc(n);
-  cand_sizes<<<ceil_div(n, 128), 128, 0, s>>>(n, own, far, L.il_ptr.get(), L.il_idx.get(), own_b.get(),
-                                              own_len.get(), far_len.get());
+  own_b.alloc(std::max<int64_t>(n, 1));
+  own_len.alloc(std::max<int64_t>(n, 1));
+  far_len.alloc(std::max<int64_t>(n, 1));
+  if (n)
+    cand_sizes<<<ceil_div(n, 128), 128, 0, s>>>(n, own, far, L.il_ptr.get(), L.il_idx.get(), own_b.get(),
+                                                own_len.get(), far_len.get());
   CKL();
-  auto ob = to_host(own_b.get(), n, s), ol = to_host(own_len.get(), n, s), fl = to_host(far_len.get(), n, s);
-  std::vector<int64_t> mh(n), nh(n), caph(n), u_off(n), v_off(n), f_off(n), piv_off(n), mat_off(n), far_off(n);
+  auto ol = to_host(own_len.get(), n, s), fl = to_host(far_len.get(), n, s);
+  std::vector<int64_t> mh(n), nh(n), caph(n), piv_off(n), mat_off(n), order(n);
+  int64_t m_max = 1, n_max = 1, f_max = 1, cap_max = 1;
   for (int64_t c = 0; c < n; c++) {
     mh[c] = rows_far ? fl[c] : ol[c];
     nh[c] = rows_far ? ol[c] : fl[c];
     int64_t cp = std::min(mh[c], nh[c]);
     if (max_rank >= 0) cp = std::min(cp, max_rank);
     caph[c] = cp;
+    m_max = std::max(m_max, mh[c]);
+    n_max = std::max(n_max, nh[c]);
+    f_max = std::max(f_max, fl[c]);
+    cap_max = std::max(cap_max, cp);
   }
-  // offsets: pivots and interpolation matrices for the whole level
   int64_t po = 0, mo = 0;
   for (int64_t c = 0; c < n; c++) {
     piv_off[c] = po;
@@ -526,128 +1000,126 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
     mat_off[c] = mo;
     mo += (which_interp == 0 ? mh[c] : nh[c]) * caph[c];
   }
+  for (int64_t c = 0; c < n; c++) order[c] = c;
+  std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) {
+    return (mh[x] + nh[x]) * caph[x] > (mh[y] + nh[y]) * caph[y];
+  });
   R.piv_off = upload(piv_off, s);
-  R.rank.alloc(n);
-  R.conv.alloc(n);
-  R.nevals.alloc(n);
-  DBuf<int64_t> rp, cp;
-  rp.alloc(std::max<int64_t>(po, 1));
-  cp.alloc(std::max<int64_t>(po, 1));
+  R.rank.alloc(std::max<int64_t>(n, 1));
+  R.conv.alloc(std::max<int64_t>(n, 1));
+  R.nevals.alloc(std::max<int64_t>(n, 1));
   R.tpiv.alloc(std::max<int64_t>(po, 1));
   R.spiv.alloc(std::max<int64_t>(po, 1));
   R.mat_off = upload(mat_off, s);
   R.mat_rows = upload(which_interp == 0 ? mh : nh, s);
   R.mat.alloc(std::max<int64_t>(mo, 1));
-  auto d_m = upload(mh, s), d_n = upload(nh, s), d_cap = upload(caph, s);
-  auto d_ob = upload(ob, s);
-  // batches bounded by the workspace budget
-  const size_t budget = workspace_budget();
-  int64_t c0 = 0;
-  while (c0 < n) {
-    size_t bytes = 0;
-    int64_t far_tot = 0, ws_u = 0, ws_v = 0, ws_f = 0, maxcap = 0;
-    int64_t c1 = c0;
-    while (c1 < n) {
-      size_t cb = (size_t)((mh[c1] + nh[c1]) * caph[c1]) * 8 + (size_t)(mh[c1] + nh[c1]) + (size_t)fl[c1] * (D * 8 + 8);
-      if (c1 > c0 && bytes + cb > budget) break;
-      bytes += cb;
-      u_off[c1] = ws_u;
-      v_off[c1] = ws_v;
-      f_off[c1] = ws_f;
-      far_off[c1] = far_tot;
-      ws_u += mh[c1] * caph[c1];
-      ws_v += nh[c1] * caph[c1];
-      ws_f += mh[c1] + nh[c1];
-      far_tot += fl[c1];
-      maxcap = std::max(maxcap, caph[c1]);
-      c1++;
-    }
-    const int64_t nb = c1 - c0;
-    DBuf<double> U, V, farc;
-    DBuf<unsigned char> flags;
-    DBuf<int64_t> farg;
-    U.alloc(std::max<int64_t>(ws_u, 1));
-    V.alloc(std::max<int64_t>(ws_v, 1));
-    flags.alloc(std::max<int64_t>(ws_f, 1));
-    farc.alloc(std::max<int64_t>(far_tot * D, 1));
-    farg.alloc(std::max<int64_t>(far_tot, 1));
-    std::vector<int64_t> sl_u(u_off.begin(), u_off.end()), sl_v(v_off.begin(), v_off.end());
-    auto d_uoff = upload(u_off, s), d_voff = upload(v_off, s), d_foff = upload(f_off, s),
-         d_faroff = upload(far_off, s);
-    gather_far<D><<<(unsigned)nb, 128, 0, s>>>(c0, far, L.il_ptr.get(), L.il_idx.get(), d_faroff.get(), farc.get(),
-                                               std::max<int64_t>(far_tot, 1), farg.get());
-    CKL();
-    AcaArgs A;
-    A.kind = kind;
-    A.a = a;
-    A.eps2 = eps * eps;
-    A.cell0 = c0;
-    A.m = d_m.get();
-    A.n = d_n.get();
-    A.cap = d_cap.get();
-    if (rows_far) {
-      A.row_base = farc.get();
-      A.ld_row = std::max<int64_t>(far_tot, 1);
-      A.row_off = d_faroff.get();
-      A.row_gidx = farg.get();
-      A.col_base = own.coords;
-      A.ld_col = own.ld;
-      A.col_off = d_ob.get();
-      A.col_gidx = own.gidx;
-    } else {
-      A.row_base = own.coords;
-      A.ld_row = own.ld;
-      A.row_off = d_ob.get();
-      A.row_gidx = own.gidx;
-      A.col_base = farc.get();
-      A.ld_col = std::max<int64_t>(far_tot, 1);
-      A.col_off = d_faroff.get();
-      A.col_gidx = farg.get();
-    }
-    A.U = U.get();
-    A.u_off = d_uoff.get();
-    A.V = V.get();
-    A.v_off = d_voff.get();
-    A.flags = flags.get();
-    A.f_off = d_foff.get();
-    A.piv_off = R.piv_off.get();
-    A.rp = rp.get();
-    A.cp = cp.get();
-    A.tpiv = R.tpiv.get();
-    A.spiv = R.spiv.get();
-    A.rank = R.rank.get();
-    A.conv = R.conv.get();
-    A.nevals = R.nevals.get();
-    size_t smem = (size_t)std::max<int64_t>(maxcap, 1) * 4 * sizeof(double);
-    if (smem > 200 * 1024) throw std::runtime_error("ACA rank cap too large for shared memory");
-    {
-      // optional: cap CTAs per SM so the per-cell V working sets stay L2-resident
-      static const long pad = [] {
-        const char* e = getenv("H2B_ACA_SMEM_KB");
-        return e ? atol(e) : 0L;
-      }();
-      if (pad > 0) smem = std::max<size_t>(smem, (size_t)pad * 1024);
-    }
-    int64_t nsum = 0;
-    for (int64_t c = c0; c < c1; c++) nsum += std::max(mh[c], nh[c]);
-    if (nsum < 2048 * nb) {
-      set_aca_smem<D, 128>(smem);
-      aca_kernel<D, 128><<<(unsigned)nb, 128, smem, s>>>(A);
-    } else {
-      set_aca_smem<D, 256>(smem);
-      aca_kernel<D, 256><<<(unsigned)nb, 256, smem, s>>>(A);
-    }
-    CKL();
-    if (which_interp == 0)
-      interp_kernel<<<(unsigned)nb, 256, 0, s>>>(0, c0, d_m.get(), R.rank.get(), U.get(), d_uoff.get(), rp.get(),
-                                                 R.piv_off.get(), R.mat.get(), R.mat_off.get());
-    else
-      interp_kernel<<<(unsigned)nb, 256, 0, s>>>(1, c0, d_n.get(), R.rank.get(), V.get(), d_voff.get(), cp.get(),
-                                                 R.piv_off.get(), R.mat.get(), R.mat_off.get());
-    CKL();
-    CK(cudaStreamSynchronize(s));
-    c0 = c1;
+  if (n == 0) {
+    R.rank_h.clear();
+    return;
   }
+  // Cells whose ACA factors fit in shared memory run in a U,V-in-smem launch; the rest keep U (cap x m) in
+  // shared memory when it fits and V in the per-CTA global slab.
+  const int64_t sm_budget = H2B_ACA_VSMEM_KB * 1024 / 8 - (4 + 32) * cap_max;  // + per-warp cross partials
+#ifdef H2B_ACA_NO_USMEM
+  const int64_t u_budget = 0;
+#else
+  const int64_t u_budget = sm_budget;
+#endif
+  std::vector<int64_t> small, mid, large;
+  for (int64_t c : order) {
+    if (caph[c] * (nh[c] + mh[c]) <= sm_budget) small.push_back(c);
+    else if (caph[c] * mh[c] <= u_budget) mid.push_back(c);
+    else large.push_back(c);
+  }
+  auto d_cap = upload(caph, s);
+  auto d_small = upload(small, s), d_mid = upload(mid, s), d_large = upload(large, s);
+  int dev = 0, nsm = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  CellJob J;
+  J.kind = kind;
+  J.a = a;
+  J.eps2 = eps * eps;
+  J.rows_far = rows_far ? 1 : 0;
+  J.own = own;
+  J.far = far;
+  J.il_ptr = L.il_ptr.get();
+  J.il_idx = L.il_idx.get();
+  J.caps = d_cap.get();
+  J.piv_off = R.piv_off.get();
+  J.tpiv = R.tpiv.get();
+  J.spiv = R.spiv.get();
+  J.rank = R.rank.get();
+  J.conv = R.conv.get();
+  J.nevals = R.nevals.get();
+  J.mat = R.mat.get();
+  J.mat_off = R.mat_off.get();
+  J.which = which_interp;
+  J.m_max = m_max;
+  J.f_max = f_max;
+  J.cap_max = cap_max;
+  static const bool verbose = getenv("H2B_SETUP_VERBOSE") != nullptr;
+  auto launch = [&](auto kern, int nt, const std::vector<int64_t>& cells, const DBuf<int64_t>& d_cells, bool vsmem,
+                    bool usmem) {
+    if (cells.empty()) return;
+    int64_t nmx = 1, res = 0;
+    for (int64_t c : cells) {
+      nmx = std::max(nmx, nh[c]);
+      res = std::max(res, caph[c] * ((usmem ? mh[c] : 0) + (vsmem ? nh[c] : 0)));
+    }
+    const size_t smem = (size_t)(4 * cap_max + res + (nt / 32) * cap_max) * sizeof(double);
+    if (smem > 220 * 1024) throw std::runtime_error("ACA rank cap too large for shared memory");
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, nt, smem));
+    const int64_t grid = std::min<int64_t>((int64_t)cells.size(), (int64_t)nsm * std::max(per, 1));
+    J.ncell = (int64_t)cells.size();
+    J.order = d_cells.get();
+    J.n_max = nmx;
+    int64_t ws = cap_max * m_max + cap_max * J.n_max + D * f_max + f_max + 2 * cap_max + (m_max + n_max + 7) / 8 + 1;
+    ws = (ws + 31) / 32 * 32;
+    DBuf<double> wsbuf;
+    wsbuf.alloc((size_t)(grid * ws));
+    DBuf<unsigned long long> counter;
+    counter.alloc(1);
+    CK(cudaMemsetAsync(counter.get(), 0, sizeof(unsigned long long), s));
+    J.ws = wsbuf.get();
+    J.ws_doubles = ws;
+    J.counter = counter.get();
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (verbose) {
+      CK(cudaEventCreate(&e0));
+      CK(cudaEventCreate(&e1));
+      CK(cudaEventRecord(e0, s));
+    }
+    kern<<<(unsigned)grid, nt, smem, s>>>(J);
+    CKL();
+    if (verbose) {
+      CK(cudaEventRecord(e1, s));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      fprintf(stderr, "[h2b] level %d side %d %s: %zu cells, m_max %lld n_max %lld cap_max %lld, grid %lld x %d: %.3f ms\n",
+              level, which_interp, vsmem ? "UV-smem" : (usmem ? "U-smem" : "global"), cells.size(), (long long)m_max, (long long)nmx,
+              (long long)cap_max, (long long)grid, nt, ms);
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+#ifdef H2B_ACA_PROF
+      unsigned long long pr[8];
+      CK(cudaMemcpyFromSymbol(pr, g_aca_prof, sizeof pr));
+      fprintf(stderr, "[h2b]   phase cycles (sum over CTAs, 1e6): gather %.1f row %.1f argmax %.1f norm %.1f cross %.1f col %.1f "
+              "tail %.1f interp %.1f\n", pr[0] / 1e6, pr[1] / 1e6, pr[2] / 1e6, pr[3] / 1e6, pr[4] / 1e6, pr[5] / 1e6,
+              pr[6] / 1e6, pr[7] / 1e6);
+      unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      CK(cudaMemcpyToSymbol(g_aca_prof, z, sizeof z));
+#endif
+    }
+    CK(cudaStreamSynchronize(s));  // workspace freed on return
+  };
+  launch(aca_cells<D, H2B_ACA_NT_S, CPT, true, true>, H2B_ACA_NT_S, small, d_small, true, true);
+  launch(aca_cells<D, NT, CPT, false, true>, NT, mid, d_mid, false, true);
+  launch(aca_cells<D, NT, CPT, false, false>, NT, large, d_large, false, false);
+  CK(cudaStreamSynchronize(s));
   R.rank_h = to_host(R.rank.get(), n, s);
 }
 

@@ -183,6 +183,7 @@ int h2b_tree_build(const double* P, int64_t np, const double* Q, int64_t nq, int
   return guarded([&] {
     auto T = new h2b_tree();
     try {
+      StreamScope sc((cudaStream_t)stream);
       T->t = build_tree(P, np, Q, nq, d, shared, nu, eta, on_device != 0, (cudaStream_t)stream);
     } catch (...) {
       delete T;
@@ -244,6 +245,7 @@ int h2b_assemble(const h2b_tree* t, int kind, double a, double eps, int force_ge
     auto H = new h2b_h2();
     H->tree = const_cast<h2b_tree*>(t);
     try {
+      StreamScope sc((cudaStream_t)stream);
       H->h = assemble(*t->t, kind, a, eps, force_general != 0, max_rank, (cudaStream_t)stream);
     } catch (...) {
       delete H;
@@ -357,6 +359,7 @@ int h2b_matvec(const h2b_h2* hc, const double* w, double* u, int64_t nrhs, int o
     const DevTree& T = *h.t;
     if (nrhs < 1) throw std::invalid_argument("nrhs must be positive");
     cudaStream_t s = (cudaStream_t)stream;
+    StreamScope sc(s);
     if (on_device) {
       matvec(h, w, u, nrhs, s);
       return;
@@ -391,6 +394,7 @@ int h2b_dense_matvec(int kind, double a, const double* P, int64_t np, const doub
   return guarded([&] {
     if (!kind_valid(kind)) throw std::invalid_argument("unknown kernel kind");
     cudaStream_t s = (cudaStream_t)stream;
+    StreamScope sc(s);
     if (on_device) {
       dense_matvec(kind, a, P, np, Q, nq, d, w, u, nrhs, s);
       return;

@@ -128,6 +128,32 @@ inline unsigned ceil_div(int64_t a, int64_t b) { return (unsigned)((a + b - 1) /
 // grid size for a bounds-checked 1D kernel: never 0 (a 0-block launch is an error)
 inline unsigned nblk(int64_t n, int64_t b) { return n > 0 ? ceil_div(n, b) : 1u; }
 
+// Stream-ordered allocation: every DBuf is carved from the device's default
+// memory pool (cudaMallocAsync) on the stream of the current API call, and
+// the pool keeps freed memory cached (release threshold = max), so the many
+// short-lived workspaces of the setup cost no cudaMalloc/cudaFree round trips.
+inline cudaStream_t& alloc_stream() {
+  static thread_local cudaStream_t s = 0;
+  return s;
+}
+struct StreamScope {
+  cudaStream_t prev;
+  explicit StreamScope(cudaStream_t s) : prev(alloc_stream()) { alloc_stream() = s; }
+  ~StreamScope() { alloc_stream() = prev; }
+};
+inline void pool_init() {
+  static const bool done = [] {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    return true;
+  }();
+  (void)done;
+}
+
 // Device buffer with byte accounting.
 struct MemStats {
   int64_t bytes = 0;
@@ -156,13 +182,14 @@ struct DBuf {
     n = count;
     ms = stats;
     if (count) {
-      CK(cudaMalloc(&p, count * sizeof(T)));
+      pool_init();
+      CK(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), alloc_stream()));
       if (ms) ms->bytes += (int64_t)(count * sizeof(T));
     }
   }
   void release() {
     if (p) {
-      cudaFree(p);
+      cudaFreeAsync(p, alloc_stream());
       if (ms) ms->bytes -= (int64_t)(n * sizeof(T));
     }
     p = nullptr;

@@ -264,6 +264,35 @@ __global__ void build_lists(int pass, int level, int64_t n, const unsigned long 
   }
 }
 
+// Sort every (short) list segment by its row-major key: one warp per segment,
+// keys staged in shared memory, each element placed at its rank (keys within a
+// segment are distinct cell keys).  Replaces a segmented radix sort whose
+// launch overhead dominated for ~100-entry segments.
+constexpr int SEG_SMAX = 512;  // longest segment handled here (longer -> CUB)
+__global__ void rank_sort_segments(int64_t nseg, const int64_t* __restrict__ ptr, const int64_t* __restrict__ key,
+                                   const int64_t* __restrict__ val, int64_t* __restrict__ out) {
+  __shared__ int64_t ks[4][SEG_SMAX];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t seg = blockIdx.x * 4 + w;
+  if (seg >= nseg) return;
+  const int64_t b = ptr[seg], len = ptr[seg + 1] - b;
+  for (int64_t i = lane; i < len; i += 32) ks[w][i] = key[b + i];
+  __syncwarp();
+  for (int64_t i = lane; i < len; i += 32) {
+    const int64_t ki = ks[w][i];
+    int r = 0;
+    for (int64_t j = 0; j < len; j++) r += ks[w][j] < ki || (ks[w][j] == ki && j < i);
+    out[b + r] = val[b + i];
+  }
+}
+
+__global__ void max_seg_len(int64_t n, const int64_t* __restrict__ ptr, int* __restrict__ mx) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const int64_t len = ptr[c + 1] - ptr[c];
+  atomicMax(mx, len > (1 << 30) ? (1 << 30) : (int)len);
+}
+
 struct Cub {
   DBuf<unsigned char> tmp;
   void ensure(size_t bytes) {
@@ -557,6 +586,19 @@ void build_tree_impl(DevTree& T, const double* Pd, const double* Qd, cudaStream_
     for (int which = 0; which < 2; which++) {
       int64_t tot = which ? V.il_total : V.nb_total;
       if (!tot) continue;
+      const int64_t* sp = which ? V.il_ptr.get() : V.nb_ptr.get();
+      DBuf<int> mx;
+      mx.alloc(1);
+      CK(cudaMemsetAsync(mx.get(), 0, sizeof(int), s));
+      max_seg_len<<<nblk(V.n, 256), 256, 0, s>>>(V.n, sp, mx.get());
+      CKL();
+      if (read_one(mx.get(), s) <= SEG_SMAX) {
+        rank_sort_segments<<<ceil_div(V.n, 4), 128, 0, s>>>(V.n, sp, which ? ilk.get() : nbk.get(),
+                                                             which ? ili.get() : nbi.get(),
+                                                             which ? V.il_idx.get() : V.nb_idx.get());
+        CKL();
+        continue;
+      }
       DBuf<int64_t> ksorted;
       ksorted.alloc(tot);
       const int64_t* ptr = which ? V.il_ptr.get() : V.nb_ptr.get();

@@ -548,6 +548,7 @@ struct CellJob {
   double* ws;
   int64_t ws_doubles;  // per CTA
   int64_t m_max, n_max, f_max, cap_max;
+  int64_t u_slab, v_slab;  // doubles reserved per CTA for U / V (0 when they live in shared memory)
   unsigned long long* counter;
 };
 
@@ -570,8 +571,8 @@ __global__ void __launch_bounds__(NT, VSMEM ? 1 : H2B_ACA_MINB) aca_cells(CellJo
   double* crossu = sm + 3 * J.cap_max;
   double* base = J.ws + (int64_t)blockIdx.x * J.ws_doubles;
   double* Ub = base;
-  double* Vb = Ub + J.cap_max * J.m_max;
-  double* FC = Vb + J.cap_max * J.n_max;
+  double* Vb = Ub + J.u_slab;
+  double* FC = Vb + J.v_slab;
   int64_t* FG = reinterpret_cast<int64_t*>(FC + D * J.f_max);
   int64_t* RP = FG + J.f_max;
   int64_t* CP = RP + J.cap_max;
@@ -720,36 +721,48 @@ __global__ void __launch_bounds__(NT, VSMEM ? 1 : H2B_ACA_MINB) aca_cells(CellJo
           const int j0 = jb + tid;
           double acc[CPT], vl[CPT];
           int jc[CPT];
+          // all loads of the iteration head first (coordinates, raw row k - 1), then the arithmetic
+          double y[CPT][D], raw[CPT];
 #pragma unroll
           for (int c = 0; c < CPT; c++) {
             const int jj = j0 + c * NT;
             jc[c] = jj < ni ? jj : 0;
-            double y[D];
 #pragma unroll
-            for (int q = 0; q < D; q++) y[q] = colc(q, jc[c]);
-            acc[c] = kval_exact(J.kind, J.a, r2_exact<D>(xl, y));
+            for (int q = 0; q < D; q++) y[c][q] = colc(q, jc[c]);
+            raw[c] = fuse ? Vlast[jc[c]] : 0.0;
+          }
+#pragma unroll
+          for (int c = 0; c < CPT; c++) {
+            const int jj = j0 + c * NT;
+            acc[c] = kval_exact(J.kind, J.a, r2_exact<D>(xl, y[c]));
             vl[c] = 0.0;
             if (fuse && jj < ni) {  // normalise row k - 1 in passing
-              vl[c] = __ddiv_rn(Vlast[jj], piv_prev);
+              vl[c] = __ddiv_rn(raw[c], piv_prev);
               Vlast[jj] = vl[c];
               v2p += vl[c] * vl[c];
             }
           }
           const double* Vt = V;
           if (fuse) {
+            // rows t < k - 1 in blocks of 4: all 4 x CPT loads issued before the dependent arithmetic
             for (int t0 = 0; t0 < kf; t0 += 4, Vt += 4 * (int64_t)n) {
+              double v[4][CPT];
+              const bool full4 = t0 + 4 <= kf;
+#pragma unroll
+              for (int tt = 0; tt < 4; tt++)
+#pragma unroll
+                for (int c = 0; c < CPT; c++)
+                  v[tt][c] = (full4 || t0 + tt < kf) ? Vt[(int64_t)tt * n + jc[c]] : 0.0;
               double p[4];
 #pragma unroll
               for (int tt = 0; tt < 4; tt++) {
                 p[tt] = 0.0;
-                if (t0 + tt < kf) {
+                if (full4 || t0 + tt < kf) {
                   const double ut = urow[t0 + tt];
-                  const double* Vr = Vt + (int64_t)tt * n;
 #pragma unroll
                   for (int c = 0; c < CPT; c++) {
-                    const double v = Vr[jc[c]];
-                    acc[c] = __dsub_rn(acc[c], __dmul_rn(ut, v));
-                    p[tt] = fma(v, vl[c], p[tt]);
+                    acc[c] = __dsub_rn(acc[c], __dmul_rn(ut, v[tt][c]));
+                    p[tt] = fma(v[tt][c], vl[c], p[tt]);
                   }
                 }
               }
@@ -769,8 +782,21 @@ __global__ void __launch_bounds__(NT, VSMEM ? 1 : H2B_ACA_MINB) aca_cells(CellJo
 #pragma unroll
             for (int c = 0; c < CPT; c++) acc[c] = __dsub_rn(acc[c], __dmul_rn(urow[ki - 1], vl[c]));
           } else {
-#pragma unroll 4
-            for (int t = 0; t < ki; t++, Vt += ni) {
+            int t = 0;
+            for (; t + 4 <= ki; t += 4, Vt += 4 * (int64_t)n) {
+              double v[4][CPT];
+#pragma unroll
+              for (int tt = 0; tt < 4; tt++)
+#pragma unroll
+                for (int c = 0; c < CPT; c++) v[tt][c] = Vt[(int64_t)tt * n + jc[c]];
+#pragma unroll
+              for (int tt = 0; tt < 4; tt++) {
+                const double ut = urow[t + tt];
+#pragma unroll
+                for (int c = 0; c < CPT; c++) acc[c] = __dsub_rn(acc[c], __dmul_rn(ut, v[tt][c]));
+              }
+            }
+            for (; t < ki; t++, Vt += ni) {
               const double ut = urow[t];
 #pragma unroll
               for (int c = 0; c < CPT; c++) acc[c] = __dsub_rn(acc[c], __dmul_rn(ut, Vt[jc[c]]));
@@ -953,7 +979,7 @@ struct SideResult {
 };
 
 #ifndef H2B_ACA_NT
-#define H2B_ACA_NT 1024
+#define H2B_ACA_NT 512
 #endif
 #ifndef H2B_ACA_CPT
 #define H2B_ACA_CPT 4
@@ -968,6 +994,7 @@ struct SideResult {
 template <int D>
 void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const Src& far, int kind, double a,
               double eps, int64_t max_rank, int which_interp, SideResult& R, cudaStream_t s) {
+  const auto wall0 = std::chrono::steady_clock::now();
   constexpr int NT = H2B_ACA_NT, CPT = H2B_ACA_CPT;
   const DevLevel& L = T.lv[level];
   const int64_t n = L.n;
@@ -1076,7 +1103,14 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
     J.ncell = (int64_t)cells.size();
     J.order = d_cells.get();
     J.n_max = nmx;
-    int64_t ws = cap_max * m_max + cap_max * J.n_max + D * f_max + f_max + 2 * cap_max + (m_max + n_max + 7) / 8 + 1;
+    int64_t us = 0, vs = 0;
+    for (int64_t c : cells) {
+      us = std::max(us, caph[c] * mh[c]);
+      vs = std::max(vs, caph[c] * nh[c]);
+    }
+    J.u_slab = usmem ? 0 : us;
+    J.v_slab = vsmem ? 0 : vs;
+    int64_t ws = J.u_slab + J.v_slab + D * f_max + f_max + 2 * cap_max + (m_max + n_max + 7) / 8 + 1;
     ws = (ws + 31) / 32 * 32;
     DBuf<double> wsbuf;
     wsbuf.alloc((size_t)(grid * ws));
@@ -1121,6 +1155,9 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
   launch(aca_cells<D, NT, CPT, false, false>, NT, large, d_large, false, false);
   CK(cudaStreamSynchronize(s));
   R.rank_h = to_host(R.rank.get(), n, s);
+  if (getenv("H2B_SETUP_VERBOSE"))
+    fprintf(stderr, "[h2b] level %d side %d: run_side wall %.3f ms\n", level, which_interp,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count());
 }
 
 template <int D>
@@ -1219,6 +1256,13 @@ std::unique_ptr<DevH2> assemble_impl(const DevTree& T, int kind, double a, doubl
     }
     H->cells_visited += HL.n;
   }
+  static const bool verbose = getenv("H2B_SETUP_VERBOSE") != nullptr;
+  auto stamp = [&](const char* what) {
+    if (verbose)
+      fprintf(stderr, "[h2b] assemble %s at %.3f ms\n", what,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  };
+  stamp("levels done");
   // coupling / near-field entry counts (what the reference would evaluate)
   {
     DBuf<unsigned long long> acc;
@@ -1241,8 +1285,10 @@ std::unique_ptr<DevH2> assemble_impl(const DevTree& T, int kind, double a, doubl
     CKL();
     H->evals_nearfield = (int64_t)read_one(acc.get(), s);
   }
+  stamp("counts done");
   prepare_matvec(*H, s);  // interaction work list + scratch are part of the setup
   CK(cudaStreamSynchronize(s));
+  stamp("matvec prepared");
   H->setup_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
   return H;
 }

@@ -235,23 +235,22 @@ struct WarpSmem {
 // concatenation into one stage (whole warp; lane 0 arms the mbarrier first).
 template <int W>
 __device__ __forceinline__ void issue_tile(const double2* rec, int nmem, const int* pref, const int* sbeg,
-                                           int p0, int cnt, double2* dst, uint64_t* bar) {
+                                           int p0, int cnt, double2* dst, uint64_t* bar, int& lo) {
   const int lane = threadIdx.x & 31;
   if (lane == 0) mbar_expect_tx(bar, (uint32_t)cnt * (uint32_t)(W * 16));
   __syncwarp();
-  int lo = 0, hi = nmem;  // last member with pref[q] <= p0
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (pref[mid] <= p0) lo = mid;
-    else hi = mid;
-  }
+  // windows advance monotonically: lo (warp-uniform) = a member at or before the one holding p0
+  while (pref[lo + 1] <= p0) lo++;
   const int p1 = p0 + cnt;
+  int last = lo;
   for (int qm = lo + lane; qm < nmem && pref[qm] < p1; qm += 32) {
     const int pa = pref[qm] > p0 ? pref[qm] : p0;
     const int pb = pref[qm + 1] < p1 ? pref[qm + 1] : p1;
+    last = qm;
     if (pb > pa)
       bulk_g2s(dst + (pa - p0) * W, rec + (int64_t)(sbeg[qm] + (pa - pref[qm])) * W, (uint32_t)(pb - pa) * (W * 16), bar);
   }
+  lo = __reduce_max_sync(0xffffffffu, last);  // the member holding the end of this window
 }
 
 // Stream the concatenated source ranges of nmem list members (sbeg / pref in
@@ -268,7 +267,8 @@ __device__ __forceinline__ void stream_members(WarpSmem<D, NR, TILE, RT>& S, con
   const int total = S.pref[nmem];
   if (total == 0) return;
   const int ntiles = (total + TILE - 1) / TILE;
-  issue_tile<W>(rec, nmem, S.pref, S.sbeg, 0, total < TILE ? total : TILE, S.stage[ntile & 1], &S.bar[ntile & 1]);
+  int lo = 0;  // issue cursor over the members
+  issue_tile<W>(rec, nmem, S.pref, S.sbeg, 0, total < TILE ? total : TILE, S.stage[ntile & 1], &S.bar[ntile & 1], lo);
   for (int it = 0; it < ntiles; it++, ntile++) {
     const int b = ntile & 1;
     const int p0 = it * TILE;
@@ -301,7 +301,7 @@ __device__ __forceinline__ void stream_members(WarpSmem<D, NR, TILE, RT>& S, con
     if (it + 1 < ntiles) {
       const int q0 = p0 + TILE;
       issue_tile<W>(rec, nmem, S.pref, S.sbeg, q0, total - q0 < TILE ? total - q0 : TILE, S.stage[b ^ 1],
-                    &S.bar[b ^ 1]);
+                    &S.bar[b ^ 1], lo);
     }
     if (worker) {
 #pragma unroll (UNROLL_J)

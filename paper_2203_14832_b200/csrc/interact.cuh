@@ -470,7 +470,7 @@ __device__ __forceinline__ void interact_cell(const LevelTab& T, int64_t c, int6
 // Persistent kernel: every warp pulls work items (descending pair count) from
 // a global counter until the list is exhausted.
 template <int D, int KIND, int NR, int TILE, int RT>
-__global__ void __launch_bounds__(IT2, H2B_MINB) interact_warps(const int64_t* __restrict__ items, int64_t n_items,
+__global__ void __launch_bounds__(IT2, NR == 1 ? H2B_MINB : 2) interact_warps(const int64_t* __restrict__ items, int64_t n_items,
                                                       unsigned long long* __restrict__ counter,
                                                       const LevelTab* __restrict__ tabs, int ntabs, int near_list,
                                                       int64_t R, int64_t r0, KParams kp) {

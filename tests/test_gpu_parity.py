@@ -237,6 +237,26 @@ def test_linearity_and_multirhs(h2c):
     assert np.linalg.norm(U[rows, 0] - exact) / np.linalg.norm(exact) <= 1e-7
 
 
+def test_multirhs_chunks_match_columns(h2c, oracle_mod):
+    """17 right-hand sides = one 16-wide chunk (multi-RHS interaction kernel) + one single column."""
+    from paper_2203_14832_b200 import sampling
+
+    pts = sampling.uniform_points(12000, 2, 4)
+    cloud = h2c.PointCloud.from_points(pts)
+    tree = h2c.build_tree(cloud, nu=64, eta=float(np.sqrt(2.0)))
+    k = h2c.builtin_kernel("coulomb-3d", 2)
+    h2 = h2c.assemble(tree, k, 1e-10)
+    W = np.random.default_rng(5).standard_normal((12000, 17))
+    U = h2c.h2_matvec(h2, W)
+    for r in (0, 7, 15, 16):
+        ur = h2c.h2_matvec(h2, W[:, r])
+        assert np.allclose(U[:, r], ur, rtol=0, atol=1e-13 * np.abs(ur).max())
+    ot = oracle_mod.OTree(pts, None, nu=64)
+    oh = oracle_mod.OH2(ot, k.kind, k.device_param, 1e-10)
+    Uo = oh.matvec(W)
+    assert np.linalg.norm(U - Uo) / np.linalg.norm(Uo) <= 1e-10
+
+
 def test_device_tensor_path(h2c):
     import torch
 

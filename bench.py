@@ -238,15 +238,21 @@ def run_b200(args, cfg, world, rank, local):
     wcloud = h2c.PointCloud.from_points(pts[:: max(1, n // 4096)][:4096])
     h2c.h2_matvec(h2c.assemble(h2c.build_tree(wcloud, nu=nu, eta=float(np.sqrt(2.0))), kern, eps),
                   np.ones(wcloud.n_sources))
-    # ---- setup: tree + NNCA (timed on the host around synchronous calls) ----
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    tree = h2c.build_tree(cloud, nu=nu, eta=float(np.sqrt(2.0)))
-    t1 = time.perf_counter()
-    h2 = h2c.assemble(tree, kern, eps)
-    torch.cuda.synchronize()
-    t2 = time.perf_counter()
-    tree_ms, nnca_ms = 1e3 * (t1 - t0), 1e3 * (t2 - t1)
+    # ---- setup: tree + NNCA (timed on the host around synchronous calls).  Run twice: the first full-size
+    # setup also grows the stream-ordered memory pool and loads the large-cell kernel variants the small
+    # warm-up did not touch (reported as setup_first_ms); the second is the steady state (setup_ms). ----
+    setups = []
+    for _ in range(2):
+        h2 = tree = None
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        tree = h2c.build_tree(cloud, nu=nu, eta=float(np.sqrt(2.0)))
+        t1 = time.perf_counter()
+        h2 = h2c.assemble(tree, kern, eps)
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        setups.append((1e3 * (t1 - t0), 1e3 * (t2 - t1)))
+    tree_ms, nnca_ms = setups[-1]
 
     stream = torch.cuda.current_stream(dev)
     wd = torch.from_numpy(np.ascontiguousarray(w)).to(dev)
@@ -319,6 +325,7 @@ def run_b200(args, cfg, world, rank, local):
         "config": {"workload": workload_name(args, cfg, n), "N": n, "nrhs": nrhs,
                    "l2": "flushed (256 MB write) between timed steps", "parallelism": f"replicas x{world}"},
         "matvec_ms": ms, "setup_ms": tree_ms + nnca_ms, "tree_ms": tree_ms, "nnca_ms": nnca_ms,
+        "setup_first_ms": sum(setups[0]),
         "depth": int(st[8]), "max_rank": int(st[3]), "m2l_pairs": pairs_m2l, "p2p_pairs": pairs_p2p,
         "stage_ms": {"upward": stage[0], "m2l": stage[1], "l2l": stage[2], "near_l2p": stage[3], "total": stage[4]},
         "rel_l2_err_dense_1000_rows": err_dense,

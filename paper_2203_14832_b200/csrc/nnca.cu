@@ -42,6 +42,9 @@ namespace {
 #ifndef H2B_ACA_SLAB_GB
 #define H2B_ACA_SLAB_GB 24
 #endif
+#ifndef H2B_ACA_SLAB_PAD
+#define H2B_ACA_SLAB_PAD 544
+#endif
 #ifndef H2B_ACA_NT_S
 #define H2B_ACA_NT_S 512
 #endif
@@ -1366,6 +1369,19 @@ struct SideResult {
   DBuf<int64_t> mat_off, mat_rows;
 };
 
+// Process-wide ACA workspace arena: grows to the largest launch seen and is
+// reused after that, so repeated setups do not churn the allocator (pool
+// growth in the middle of a setup made some runs 2-3x slower).
+double* aca_arena(size_t doubles, cudaStream_t s) {
+  static DBuf<double> arena;
+  if (arena.n < doubles) {
+    CK(cudaStreamSynchronize(s));
+    arena.release();
+    arena.alloc(doubles + doubles / 8);
+  }
+  return arena.get();
+}
+
 template <int D>
 void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const Src& far, int kind, double a,
               double eps, int64_t max_rank, int which_interp, SideResult& R, cudaStream_t s) {
@@ -1486,13 +1502,12 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
     J.u_slab = usmem ? 0 : us;
     J.v_slab = vsmem ? 0 : vs;
     int64_t ws = J.u_slab + J.v_slab + D * f_max + f_max + 2 * cap_max + (m_max + n_max + 7) / 8 + 1;
-    ws = (ws + 31) / 32 * 32;
-    DBuf<double> wsbuf;
-    wsbuf.alloc((size_t)(grid * ws));
+    ws = (ws + 31) / 32 * 32 + H2B_ACA_SLAB_PAD;  // pad: per-CTA slabs off power-of-two strides
+    double* wsbuf = aca_arena((size_t)(grid * ws), s);
     DBuf<unsigned long long> counter;
     counter.alloc(1);
     CK(cudaMemsetAsync(counter.get(), 0, sizeof(unsigned long long), s));
-    J.ws = wsbuf.get();
+    J.ws = wsbuf;
     J.ws_doubles = ws;
     J.counter = counter.get();
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -1523,7 +1538,6 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
       CK(cudaMemcpyToSymbol(g_aca_prof, z, sizeof z));
 #endif
     }
-    CK(cudaStreamSynchronize(s));  // workspace freed on return
   };
 #ifdef H2B_ACA_WARPS
   {
@@ -1547,14 +1561,13 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
     const int64_t budget = (int64_t)H2B_ACA_SLAB_GB << 27;  // doubles
     int64_t blocks = std::min<int64_t>((int64_t)nsm * std::max(per, 1), (n + 7) / 8);
     blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, budget / (8 * ws)));
-    DBuf<double> wsbuf;
-    wsbuf.alloc((size_t)(blocks * 8 * ws));
+    double* wsbuf = aca_arena((size_t)(blocks * 8 * ws), s);
     DBuf<unsigned long long> counter;
     counter.alloc(1);
     CK(cudaMemsetAsync(counter.get(), 0, sizeof(unsigned long long), s));
     J.ncell = n;
     J.order = d_order_all.get();
-    J.ws = wsbuf.get();
+    J.ws = wsbuf;
     J.ws_doubles = ws;
     J.counter = counter.get();
     kern<<<(unsigned)blocks, 256, smem, s>>>(J);
@@ -1585,6 +1598,7 @@ std::unique_ptr<DevH2> assemble_impl(const DevTree& T, int kind, double a, doubl
   H->symmetric = T.shared && !force_general;  // all built-in kernels are symmetric
   const int L = T.depth;
   H->lv.resize(L + 1);
+  std::vector<std::vector<int64_t>> kin_h(L + 1);
   for (int level = L; level >= 2; level--) {
     const DevLevel& Lv = T.lv[level];
     DevH2Level& HL = H->lv[level];
@@ -1606,9 +1620,13 @@ std::unique_ptr<DevH2> assemble_impl(const DevTree& T, int kind, double a, doubl
     SideResult in;
     run_side<D>(T, level, false, own_t, far_s, kind, a, eps, max_rank, 0, in, s);
     HL.kin = std::move(in.rank);
-    HL.in_ptr.alloc(HL.n + 1, &H->mem);
-    excl_scan(HL.kin.get(), HL.n, HL.in_ptr.get(), s);
-    HL.in_total = read_one(HL.in_ptr.get() + HL.n, s);
+    {  // pivot offsets from the ranks already on the host (no device scan + read-back)
+      std::vector<int64_t> ptr(HL.n + 1, 0);
+      for (int64_t c = 0; c < HL.n; c++) ptr[c + 1] = ptr[c] + in.rank_h[c];
+      HL.in_total = ptr[HL.n];
+      HL.in_ptr = upload(ptr, s, &H->mem);
+      kin_h[level] = std::move(in.rank_h);
+    }
     HL.t_in.alloc(std::max<int64_t>(HL.in_total, 1), &H->mem);
     HL.s_in.alloc(std::max<int64_t>(HL.in_total, 1), &H->mem);
     if (HL.n)
@@ -1656,18 +1674,31 @@ std::unique_ptr<DevH2> assemble_impl(const DevTree& T, int kind, double a, doubl
     } else {
       HL.out_total = HL.in_total;
     }
-    CK(cudaStreamSynchronize(s));
-    // stats
-    auto nev = to_host(HL.nevals.get(), HL.n, s);
-    auto kin = to_host(HL.kin.get(), HL.n, s);
-    auto kout = H->symmetric ? kin : to_host(HL.kout.get(), HL.n, s);
-    auto cv = to_host(HL.conv.get(), HL.n, s);
-    for (int64_t c = 0; c < HL.n; c++) {
-      H->evals_pivots += nev[c];
-      H->max_rank = std::max({H->max_rank, kin[c], kout[c]});
-      H->unconverged += cv[c] == 0;
-    }
     H->cells_visited += HL.n;
+  }
+  // stats: one batch of read-backs after all levels
+  {
+    std::vector<std::vector<int64_t>> nev(L + 1), kout(L + 1), cv(L + 1);
+    for (int level = 2; level <= L; level++) {
+      const DevH2Level& HL = H->lv[level];
+      nev[level].resize(HL.n);
+      cv[level].resize(HL.n);
+      if (!HL.n) continue;
+      CK(cudaMemcpyAsync(nev[level].data(), HL.nevals.get(), HL.n * 8, cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(cv[level].data(), HL.conv.get(), HL.n * 8, cudaMemcpyDeviceToHost, s));
+      if (!H->symmetric) {
+        kout[level].resize(HL.n);
+        CK(cudaMemcpyAsync(kout[level].data(), HL.kout.get(), HL.n * 8, cudaMemcpyDeviceToHost, s));
+      }
+    }
+    CK(cudaStreamSynchronize(s));
+    for (int level = 2; level <= L; level++)
+      for (int64_t c = 0; c < H->lv[level].n; c++) {
+        H->evals_pivots += nev[level][c];
+        H->max_rank = std::max(H->max_rank, kin_h[level][c]);
+        if (!H->symmetric) H->max_rank = std::max(H->max_rank, kout[level][c]);
+        H->unconverged += cv[level][c] == 0;
+      }
   }
   static const bool verbose = getenv("H2B_SETUP_VERBOSE") != nullptr;
   auto stamp = [&](const char* what) {

@@ -30,6 +30,9 @@ namespace {
 #ifndef H2B_ACA_NT
 #define H2B_ACA_NT 512
 #endif
+#ifndef H2B_ACA_MINB
+#define H2B_ACA_MINB 1
+#endif
 #ifndef H2B_ACA_CPT
 #define H2B_ACA_CPT 4
 #endif
@@ -578,11 +581,8 @@ struct CellJob {
   unsigned long long* counter;
 };
 
-#ifndef H2B_ACA_MINB
-#define H2B_ACA_MINB 1
-#endif
-template <int D, int NT, int CPT, bool VSMEM, bool USMEM>
-__global__ void __launch_bounds__(NT, VSMEM ? 1 : H2B_ACA_MINB) aca_cells(CellJob J) {
+template <int D, int NT, int CPT, bool VSMEM, bool USMEM, int MB>
+__global__ void __launch_bounds__(NT, MB) aca_cells(CellJob J) {
   constexpr int NW = NT / 32;
   extern __shared__ double sm[];
   __shared__ RedScratch rs;
@@ -1575,9 +1575,11 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
     CK(cudaStreamSynchronize(s));
   }
 #else
-  launch(aca_cells<D, H2B_ACA_NT_S, CPT, true, true>, H2B_ACA_NT_S, small, d_small, true, true);
-  launch(aca_cells<D, NT, CPT, false, true>, NT, mid, d_mid, false, true);
-  launch(aca_cells<D, NT, CPT, false, false>, NT, large, d_large, false, false);
+  // V in shared memory: one 512-thread CTA per SM; V in the slab: H2B_ACA_NT threads x H2B_ACA_MINB CTAs
+  // per SM (several cells in flight per SM hide the row pass's memory latency)
+  launch(aca_cells<D, H2B_ACA_NT_S, CPT, true, true, 1>, H2B_ACA_NT_S, small, d_small, true, true);
+  launch(aca_cells<D, NT, CPT, false, true, H2B_ACA_MINB>, NT, mid, d_mid, false, true);
+  launch(aca_cells<D, NT, CPT, false, false, H2B_ACA_MINB>, NT, large, d_large, false, false);
 #endif
   CK(cudaStreamSynchronize(s));
   R.rank_h = to_host(R.rank.get(), n, s);

@@ -99,6 +99,7 @@ struct DevH2 {
   std::vector<DBuf<int>> own_in, own_out;  // per level: pivot position -> owning cell
   DBuf<int> own_t;                          // sorted target position -> leaf cell
   std::vector<DBuf<double>> qmat_t;         // per level: transposed column interpolators (upward pass)
+  std::vector<int> up_sg;                   // per level: lanes per output row in the upward pass
   RecSet pack1, pack16;                     // source records for RHS chunks of width 1 / 16
   DBuf<unsigned long long> work_counter;    // persistent interaction kernel: next work item
 };

@@ -54,22 +54,58 @@ __global__ void transpose_cells(int64_t ncell, const int64_t* __restrict__ nrow,
   }
 }
 
-// upward (P2M / M2M): y[p] = sum_j AT_c[j * k + s] x_c[j],  p = out_ptr[c] + s
+// upward (P2M / M2M): y[p] = sum_j AT_c[j * k + s] x_c[j],  p = out_ptr[c] + s.
+// SG lanes share one output row (j split across them, shuffle-reduced): the
+// upper levels have few rows but long sums (nr ~ 100-200), which one thread
+// per row turns into a long dependent load chain.
+template <int SG>
 __global__ void up_rows(int64_t nout, const int* __restrict__ owner, const int64_t* __restrict__ out_ptr,
                         const int64_t* __restrict__ nrow, const double* __restrict__ A,
                         const int64_t* __restrict__ a_off, const double* __restrict__ x,
                         const int64_t* __restrict__ x_ptr, const int64_t* __restrict__ x_map,
                         double* __restrict__ y, int64_t R) {
-  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q >= nout * R) return;
-  const int64_t p = q / R, r = q - p * R;
-  const int c = owner[p];
-  const int64_t sidx = p - out_ptr[c], nr = nrow[c], k = out_ptr[c + 1] - out_ptr[c];
-  const double* As = A + a_off[c] + sidx;
-  const double* xc = x + (x_map ? x_ptr[x_map[c]] : x_ptr[c]) * R + r;
+  const int64_t qq = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t q = qq / SG;
+  const int sub = (int)(qq % SG);
+  const bool ok = q < nout * R;
   double acc = 0.0;
-  for (int64_t j = 0; j < nr; j++) acc = fma(As[j * k], xc[j * R], acc);
-  y[q] = acc;
+  if (ok) {
+    const int64_t p = q / R, r = q - p * R;
+    const int c = owner[p];
+    const int64_t sidx = p - out_ptr[c], nr = nrow[c], k = out_ptr[c + 1] - out_ptr[c];
+    const double* As = A + a_off[c] + sidx;
+    const double* xc = x + (x_map ? x_ptr[x_map[c]] : x_ptr[c]) * R + r;
+    for (int64_t j = sub; j < nr; j += SG) acc = fma(As[j * k], xc[j * R], acc);
+  }
+  if constexpr (SG > 1) {
+#pragma unroll
+    for (int o = SG / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  }
+  if (ok && sub == 0) y[q] = acc;
+}
+
+void launch_up(int sg, int64_t nout, const int* owner, const int64_t* out_ptr, const int64_t* nrow, const double* A,
+               const int64_t* a_off, const double* x, const int64_t* x_ptr, const int64_t* x_map, double* y,
+               int64_t R, cudaStream_t s) {
+  const int64_t thr = std::max<int64_t>(nout * R, 1) * sg;
+  switch (sg) {
+    case 1: up_rows<1><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R); break;
+    case 2: up_rows<2><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R); break;
+    case 4: up_rows<4><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R); break;
+    case 8: up_rows<8><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R); break;
+    default: up_rows<16><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R); break;
+  }
+  CKL();
+}
+
+// lanes per row for a level: enough rows in flight, short per-lane chains
+int up_group(int64_t rows, int64_t nr_avg) {
+  int sg = 1;
+  while (sg < 16 && (nr_avg / sg > 24 || rows * sg < 148 * 1024)) {
+    if (nr_avg / (2 * sg) < 4) break;
+    sg *= 2;
+  }
+  return sg;
 }
 
 // downward (L2L): rows of the children stacked under parent P: u_child[q] += sum_s P_P[s * nr + i] u_P[s]
@@ -317,6 +353,15 @@ void ensure_scratch(DevH2& h, int64_t R, cudaStream_t s) {
                                                         h.qmat_t[l].get());
       CKL();
     }
+    // lanes per output row of the upward pass, per level (from the mean column-interpolator height)
+    h.up_sg.assign(T.depth + 1, 1);
+    for (int l = 2; l <= T.depth; l++) {
+      const DevH2Level& HL = h.lv[l];
+      const int64_t rows = HL.out_total;
+      const int64_t nr_sum = (int64_t)(h.symmetric ? HL.pmat.n : HL.qmat.n);  // sum over cells of nr * k
+      const int64_t nr_avg = rows ? nr_sum / rows : 0;
+      h.up_sg[l] = up_group(rows, nr_avg);
+    }
     const DevLevel& Lf = T.lv[T.depth];
     h.own_t.alloc(std::max<int64_t>(T.np, 1), &h.mem);
     fill_owner<<<nblk(Lf.n, 256), 256, 0, s>>>(Lf.n, Lf.t_ptr.get(), h.own_t.get());
@@ -376,24 +421,20 @@ void matvec(DevH2& h, const double* w, double* u, int64_t R, cudaStream_t s) {
   gather_rows<<<nblk(T.nq * R, 256), 256, 0, s>>>(w, T.sperm(), T.nq, R, h.w_sorted.get());
   CKL();
   if (L >= 2) {
-    // ---- upward pass: P2M at the leaves, then M2M (one thread per output row) ----
+    // ---- upward pass: P2M at the leaves, then M2M (one or a few threads per output row) ----
     auto own_out = [&](int l) { return h.symmetric ? h.own_in[l].get() : h.own_out[l].get(); };
     {
       const DevLevel& Lv = T.lv[L];
       const DevH2Level& HL = h.lv[L];
-      up_rows<<<nblk(HL.out_total * R, 256), 256, 0, s>>>(
-          HL.out_total, own_out(L), HL.out_ptrd(), HL.n_outd(), h.qmat_t[L].get(), HL.qm_offd(), h.w_sorted.get(),
-          T.shared ? Lv.t_ptr.get() : Lv.s_ptr.get(), nullptr, h.wout[L].get(), R);
-      CKL();
+      launch_up(h.up_sg[L], HL.out_total, own_out(L), HL.out_ptrd(), HL.n_outd(), h.qmat_t[L].get(), HL.qm_offd(),
+                h.w_sorted.get(), T.shared ? Lv.t_ptr.get() : Lv.s_ptr.get(), nullptr, h.wout[L].get(), R, s);
     }
     for (int l = L - 1; l >= 2; l--) {
       const DevLevel& Lv = T.lv[l];
       const DevH2Level& HL = h.lv[l];
       const DevH2Level& HC = h.lv[l + 1];
-      up_rows<<<nblk(HL.out_total * R, 256), 256, 0, s>>>(
-          HL.out_total, own_out(l), HL.out_ptrd(), HL.n_outd(), h.qmat_t[l].get(), HL.qm_offd(), h.wout[l + 1].get(),
-          HC.out_ptrd(), Lv.ch_ptr.get(), h.wout[l].get(), R);
-      CKL();
+      launch_up(h.up_sg[l], HL.out_total, own_out(l), HL.out_ptrd(), HL.n_outd(), h.qmat_t[l].get(), HL.qm_offd(),
+                h.wout[l + 1].get(), HC.out_ptrd(), Lv.ch_ptr.get(), h.wout[l].get(), R, s);
     }
   }
   if (g_profile) CK(cudaEventRecord(ev[1], s));

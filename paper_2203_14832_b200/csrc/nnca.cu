@@ -36,6 +36,9 @@ namespace {
 #ifndef H2B_ACA_CPT
 #define H2B_ACA_CPT 4
 #endif
+#ifndef H2B_ACA_TB
+#define H2B_ACA_TB 4  // residual rows per load batch in the fused row pass
+#endif
 #ifndef H2B_ACA_WMINB
 #define H2B_ACA_WMINB 2
 #endif
@@ -770,40 +773,44 @@ __global__ void __launch_bounds__(NT, MB) aca_cells(CellJob J) {
           }
           const double* Vt = V;
           if (fuse) {
-            // rows t < k - 1 in blocks of 4: all 4 x CPT loads issued before the dependent arithmetic
-            for (int t0 = 0; t0 < kf; t0 += 4, Vt += 4 * (int64_t)n) {
-              double v[4][CPT];
-              const bool full4 = t0 + 4 <= kf;
+            // rows t < k - 1 in blocks of TB: all TB x CPT loads issued before the dependent arithmetic
+            constexpr int TB = H2B_ACA_TB;
+            for (int t0 = 0; t0 < kf; t0 += TB, Vt += TB * (int64_t)n) {
+              double v[TB][CPT];
+              const bool fullb = t0 + TB <= kf;
 #pragma unroll
-              for (int tt = 0; tt < 4; tt++)
+              for (int tt = 0; tt < TB; tt++)
 #pragma unroll
                 for (int c = 0; c < CPT; c++)
-                  v[tt][c] = (full4 || t0 + tt < kf) ? Vt[(int64_t)tt * n + jc[c]] : 0.0;
-              double p[4];
+                  v[tt][c] = (fullb || t0 + tt < kf) ? Vt[(int64_t)tt * n + jc[c]] : 0.0;
 #pragma unroll
-              for (int tt = 0; tt < 4; tt++) {
-                p[tt] = 0.0;
-                if (full4 || t0 + tt < kf) {
-                  const double ut = urow[t0 + tt];
+              for (int g4 = 0; g4 < TB; g4 += 4) {
+                double p[4];
 #pragma unroll
-                  for (int c = 0; c < CPT; c++) {
-                    acc[c] = __dsub_rn(acc[c], __dmul_rn(ut, v[tt][c]));
-                    p[tt] = fma(v[tt][c], vl[c], p[tt]);
+                for (int tt = 0; tt < 4; tt++) {
+                  p[tt] = 0.0;
+                  if (fullb || t0 + g4 + tt < kf) {
+                    const double ut = urow[t0 + g4 + tt];
+#pragma unroll
+                    for (int c = 0; c < CPT; c++) {
+                      acc[c] = __dsub_rn(acc[c], __dmul_rn(ut, v[g4 + tt][c]));
+                      p[tt] = fma(v[g4 + tt][c], vl[c], p[tt]);
+                    }
                   }
                 }
+                // transpose-reduce 4 partial sums over the warp: lane gets t = t0 + g4 + ((lane >> 3) & 3)
+                const bool b4 = lane & 16, b3 = lane & 8;
+                double k0 = b4 ? p[2] : p[0], k1 = b4 ? p[3] : p[1];
+                k0 += __shfl_xor_sync(0xffffffffu, b4 ? p[0] : p[2], 16);
+                k1 += __shfl_xor_sync(0xffffffffu, b4 ? p[1] : p[3], 16);
+                double kk = b3 ? k1 : k0;
+                kk += __shfl_xor_sync(0xffffffffu, b3 ? k0 : k1, 8);
+                kk += __shfl_xor_sync(0xffffffffu, kk, 4);
+                kk += __shfl_xor_sync(0xffffffffu, kk, 2);
+                kk += __shfl_xor_sync(0xffffffffu, kk, 1);
+                const int tq = t0 + g4 + ((lane >> 3) & 3);
+                if ((lane & 7) == 0 && tq < kf) crosspart[warp * cap + tq] += kk;
               }
-              // transpose-reduce 4 partial sums over the warp: lane gets t = t0 + ((lane >> 3) & 3)
-              const bool b4 = lane & 16, b3 = lane & 8;
-              double k0 = b4 ? p[2] : p[0], k1 = b4 ? p[3] : p[1];
-              k0 += __shfl_xor_sync(0xffffffffu, b4 ? p[0] : p[2], 16);
-              k1 += __shfl_xor_sync(0xffffffffu, b4 ? p[1] : p[3], 16);
-              double kk = b3 ? k1 : k0;
-              kk += __shfl_xor_sync(0xffffffffu, b3 ? k0 : k1, 8);
-              kk += __shfl_xor_sync(0xffffffffu, kk, 4);
-              kk += __shfl_xor_sync(0xffffffffu, kk, 2);
-              kk += __shfl_xor_sync(0xffffffffu, kk, 1);
-              const int tq = t0 + ((lane >> 3) & 3);
-              if ((lane & 7) == 0 && tq < kf) crosspart[warp * cap + tq] += kk;
             }
 #pragma unroll
             for (int c = 0; c < CPT; c++) acc[c] = __dsub_rn(acc[c], __dmul_rn(urow[ki - 1], vl[c]));

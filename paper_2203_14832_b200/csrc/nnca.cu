@@ -763,7 +763,7 @@ __global__ void __launch_bounds__(NT, MB) aca_cells(CellJob J) {
 #pragma unroll
           for (int c = 0; c < CPT; c++) {
             const int jj = j0 + c * NT;
-            acc[c] = kval_exact(J.kind, J.a, r2_exact<D>(xl, y[c]));
+            acc[c] = jj < ni ? kval_exact(J.kind, J.a, r2_exact<D>(xl, y[c])) : 0.0;  // no work on padding
             vl[c] = 0.0;
             if (fuse && jj < ni) {  // normalise row k - 1 in passing
               vl[c] = __ddiv_rn(raw[c], piv_prev);
@@ -1144,7 +1144,7 @@ __global__ void __launch_bounds__(256, H2B_ACA_WMINB) aca_warps(CellJob J) {
 #pragma unroll
           for (int c = 0; c < CPT; c++) {
             const int jj = j0 + c * 32;
-            acc[c] = kval_exact(J.kind, J.a, r2_exact<D>(xl, y[c]));
+            acc[c] = jj < ni ? kval_exact(J.kind, J.a, r2_exact<D>(xl, y[c])) : 0.0;  // no work on padding
             vl[c] = 0.0;
             if (fuse && jj < ni) {
               vl[c] = __ddiv_rn(raw[c], piv_prev);

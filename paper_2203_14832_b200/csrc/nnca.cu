@@ -1497,7 +1497,13 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, nt, smem));
-    const int64_t grid = std::min<int64_t>((int64_t)cells.size(), (int64_t)nsm * std::max(per, 1));
+    int64_t gmax = (int64_t)nsm * std::max(per, 1);
+    static const double gfrac = [] {
+      const char* e = getenv("H2B_ACA_GRID_FRAC");  // tuning: fraction of the SMs given to V-in-slab launches
+      return e ? atof(e) : 1.0;
+    }();
+    if (!vsmem && gfrac > 0 && gfrac < 1) gmax = std::max<int64_t>(1, (int64_t)(gmax * gfrac));
+    const int64_t grid = std::min<int64_t>((int64_t)cells.size(), gmax);
     J.ncell = (int64_t)cells.size();
     J.order = d_cells.get();
     J.n_max = nmx;

@@ -102,6 +102,9 @@ struct LevelTab {
   const double2* rec16;  // source records for NR = 16
   const int64_t* l_ptr;  // cell list (CSR)
   const int64_t* l_idx;
+  const int* m_sb;       // per list entry: first record of the member
+  const int* m_end;      // per list entry: inclusive prefix of member lengths within the cell's list
+                         // (near field: the cell itself counts 0, it has its own pass)
   double* out;           // result rows (target position) * R
 };
 
@@ -418,7 +421,15 @@ __device__ __forceinline__ void interact_cell_rt(const LevelTab& T, int64_t c, i
     }
     for (int64_t q0 = lb; q0 < le; q0 += MAXMEMW) {
       const int nmem = (int)(le - q0 < MAXMEMW ? le - q0 : MAXMEMW);
-      member_table<SELF>(T, c, q0, nmem, S);
+      {  // member table of this chunk from the precomputed per-entry arrays (one coalesced round trip)
+        const int base = q0 == lb ? 0 : T.m_end[q0 - 1];
+        for (int i = lane; i < nmem; i += 32) {
+          S.sbeg[i] = T.m_sb[q0 + i];
+          S.pref[i + 1] = T.m_end[q0 + i] - base;
+        }
+        if (lane == 0) S.pref[0] = 0;
+        __syncwarp();
+      }
       stream_members<D, KIND, NR, TILE, SELF, false, RT>(S, rec, nmem, o, kp, worker, grp, G, x, acc, ntile);
     }
     constexpr double SCALE = kscale<KIND>() * (is_inv_r<KIND>() ? 0.5 : 1.0);

@@ -166,6 +166,22 @@ void pack_coords(int d, const DevH2& h, int nr, cudaStream_t s) {
   }
 }
 
+// per-entry member tables of every interaction list (record start, inclusive length prefix within the
+// cell's list); the near field's own leaf counts 0 (it is handled by the r2 == 0 pass)
+__global__ void member_tables(int64_t n, const int64_t* __restrict__ l_ptr, const int64_t* __restrict__ l_idx,
+                              const int64_t* __restrict__ s_ptr, int self_zero, int* __restrict__ m_sb,
+                              int* __restrict__ m_end) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  int run = 0;
+  for (int64_t q = l_ptr[c]; q < l_ptr[c + 1]; q++) {
+    const int64_t y = l_idx[q];
+    m_sb[q] = (int)s_ptr[y];
+    run += (self_zero && y == c) ? 0 : (int)(s_ptr[y + 1] - s_ptr[y]);
+    m_end[q] = run;
+  }
+}
+
 // pair counts per work item (the reference's entry counts for S and near blocks)
 __global__ void item_costs(int64_t n, int lev, const int64_t* __restrict__ t_ptr, const int64_t* __restrict__ s_ptr,
                            const int64_t* __restrict__ l_ptr, const int64_t* __restrict__ l_idx,
@@ -280,6 +296,26 @@ void build_tabs(DevH2& h, int64_t R, cudaStream_t s) {
   const DevTree& T = *h.t;
   const int L = T.depth;
   std::vector<LevelTab> tabs(L + 2);
+  if (h.m_sb.empty()) {  // member tables (static per H2 matrix)
+    h.m_sb.resize(L + 2);
+    h.m_end.resize(L + 2);
+    std::vector<int> ids;
+    for (int l = 2; l <= L; l++) ids.push_back(l);
+    ids.push_back(L + 1);  // the near field (also when the tree has fewer than two levels)
+    for (int l : ids) {
+      const bool nf = l == L + 1;
+      const DevLevel& Lv = T.lv[nf ? L : l];
+      const int64_t tot = nf ? Lv.nb_total : Lv.il_total;
+      h.m_sb[l].alloc(std::max<int64_t>(tot, 1), &h.mem);
+      h.m_end[l].alloc(std::max<int64_t>(tot, 1), &h.mem);
+      const int64_t* sp = nf ? (T.shared ? Lv.t_ptr.get() : Lv.s_ptr.get()) : h.lv[l].out_ptrd();
+      if (Lv.n)
+        member_tables<<<nblk(Lv.n, 256), 256, 0, s>>>(Lv.n, nf ? Lv.nb_ptr.get() : Lv.il_ptr.get(),
+                                                         nf ? Lv.nb_idx.get() : Lv.il_idx.get(), sp, nf ? 1 : 0,
+                                                         h.m_sb[l].get(), h.m_end[l].get());
+      CKL();
+    }
+  }
   auto rec = [&](const RecSet& rs, int i) -> const double2* { return rs.lists.empty() ? nullptr : rs.lists[i].get(); };
   for (int l = 0; l <= L + 1; l++) {
     LevelTab& t = tabs[l];
@@ -295,6 +331,8 @@ void build_tabs(DevH2& h, int64_t R, cudaStream_t s) {
       t.rec16 = rec(h.pack16, l - 2);
       t.l_ptr = Lv.il_ptr.get();
       t.l_idx = Lv.il_idx.get();
+      t.m_sb = h.m_sb[l].get();
+      t.m_end = h.m_end[l].get();
       t.out = h.uin[l].get();
     } else if (l == L + 1) {
       const DevLevel& Lv = T.lv[L];
@@ -306,6 +344,8 @@ void build_tabs(DevH2& h, int64_t R, cudaStream_t s) {
       t.rec16 = rec(h.pack16, std::max(L - 1, 0));
       t.l_ptr = Lv.nb_ptr.get();
       t.l_idx = Lv.nb_idx.get();
+      t.m_sb = h.m_sb[L + 1].get();
+      t.m_end = h.m_end[L + 1].get();
       t.out = h.near.get();
     }
   }

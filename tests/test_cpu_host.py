@@ -88,3 +88,20 @@ def test_sampling_matches_reference_generators():
     assert np.array_equal(sampling.chebyshev_points(1024, 2, 0), g["P"])
     s = sampling.sphere_points(1000, 3, 2)
     assert np.allclose(np.linalg.norm(s, axis=1), 1.0)
+
+
+def test_bench_reference_arm_contract():
+    """bench.py --impl reference: the CPU reference path (oracle) prints one JSON line with the contract keys."""
+    import json
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(repo, "bench.py"), "--impl", "reference", "--config", "c0",
+                          "--steps", "1", "--warmup", "3"], capture_output=True, text=True, timeout=600, check=True)
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["unit"] == "N^2/s" and line["value"] > 0
+    assert line["higher_is_better"] is True and line["steps"] == 1 and line["warmup"] == 3
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
+    assert line["config"]["N"] == 4096

@@ -95,6 +95,7 @@ struct DevH2 {
   DBuf<double> near;        // near-field sums (sorted target order)
   DBuf<int64_t> items;      // interaction work list ((list << 40) | cell), by descending pair count
   int64_t n_items = 0;
+  DBuf<int> item_desc;      // per work item {first target, targets, list begin, list end} (int4)
   DBuf<unsigned char> tabs; // per-list pointer tables for the interaction kernel
   std::vector<DBuf<int>> own_in, own_out;  // per level: pivot position -> owning cell
   DBuf<int> own_t;                          // sorted target position -> leaf cell

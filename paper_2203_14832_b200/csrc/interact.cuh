@@ -371,11 +371,10 @@ __device__ __forceinline__ void member_table(const LevelTab& T, int64_t c, int64
 // path, the other neighbours (never coincident with a target) through the
 // plain path.
 template <int D, int KIND, int NR, int TILE, bool SELF, int RT, class WS>
-__device__ __forceinline__ void interact_cell_rt(const LevelTab& T, int64_t c, int64_t R, int64_t r0,
+__device__ __forceinline__ void interact_cell_rt(const LevelTab& T, int64_t c, const int4 dsc, int64_t R, int64_t r0,
                                                  const KParams& kp, WS& S, uint32_t& ntile) {
   const double2* rec = NR == 1 ? T.rec1 : T.rec16;
-  const int64_t tb = T.t_ptr[c], m = T.t_ptr[c + 1] - tb;
-  const int64_t lb = T.l_ptr[c], le = T.l_ptr[c + 1];
+  const int64_t tb = dsc.x, m = dsc.y, lb = dsc.z, le = dsc.w;  // precomputed item descriptor
   const int lane = threadIdx.x & 31;
   double o[D];
 #pragma unroll
@@ -466,23 +465,36 @@ __device__ __forceinline__ float lane_eff(int m, int rt) {
 }
 
 template <int D, int KIND, int NR, int TILE, bool SELF, class WS>
-__device__ __forceinline__ void interact_cell(const LevelTab& T, int64_t c, int64_t R, int64_t r0, const KParams& kp,
-                                              WS& S, uint32_t& ntile) {
+__device__ __forceinline__ void interact_cell(const LevelTab& T, int64_t c, const int4 dsc, int64_t R, int64_t r0,
+                                              const KParams& kp, WS& S, uint32_t& ntile) {
   if constexpr (WS::RTMAX >= 3) {
-    const int64_t m = T.t_ptr[c + 1] - T.t_ptr[c];
-    if (m <= 96 && lane_eff((int)m, 3) > lane_eff((int)m, 2)) {
-      interact_cell_rt<D, KIND, NR, TILE, SELF, 3>(T, c, R, r0, kp, S, ntile);
+    const int m = dsc.y;
+    if (m <= 96 && lane_eff(m, 3) > lane_eff(m, 2)) {
+      interact_cell_rt<D, KIND, NR, TILE, SELF, 3>(T, c, dsc, R, r0, kp, S, ntile);
       return;
     }
   }
-  interact_cell_rt<D, KIND, NR, TILE, SELF, 2>(T, c, R, r0, kp, S, ntile);
+  interact_cell_rt<D, KIND, NR, TILE, SELF, 2>(T, c, dsc, R, r0, kp, S, ntile);
+}
+
+// item descriptors {first target, targets, list begin, list end} (one 16-byte load per work item)
+__global__ void make_item_desc(const int64_t* __restrict__ items, int64_t n, const LevelTab* __restrict__ tabs,
+                               int4* __restrict__ desc) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t it = items[i];
+  const int lev = (int)(it >> 40);
+  const int64_t c = it & ((1ll << 40) - 1);
+  const LevelTab& T = tabs[lev];
+  const int64_t tb = T.t_ptr[c];
+  desc[i] = make_int4((int)tb, (int)(T.t_ptr[c + 1] - tb), (int)T.l_ptr[c], (int)T.l_ptr[c + 1]);
 }
 
 // Persistent kernel: every warp pulls work items (descending pair count) from
 // a global counter until the list is exhausted.
 template <int D, int KIND, int NR, int TILE, int RT>
-__global__ void __launch_bounds__(IT2, NR == 1 ? H2B_MINB : 2) interact_warps(const int64_t* __restrict__ items, int64_t n_items,
-                                                      unsigned long long* __restrict__ counter,
+__global__ void __launch_bounds__(IT2, NR == 1 ? H2B_MINB : 2) interact_warps(const int64_t* __restrict__ items, const int4* __restrict__ descs,
+                                                      int64_t n_items, unsigned long long* __restrict__ counter,
                                                       const LevelTab* __restrict__ tabs, int ntabs, int near_list,
                                                       int64_t R, int64_t r0, KParams kp) {
   using WS = WarpSmem<D, NR, TILE, RT>;  // RT = the largest targets-per-lane used
@@ -505,13 +517,14 @@ __global__ void __launch_bounds__(IT2, NR == 1 ? H2B_MINB : 2) interact_warps(co
     idx = __shfl_sync(0xffffffffu, idx, 0);
     if (idx >= (unsigned long long)n_items) break;
     const int64_t it = items[idx];
+    const int4 dsc = descs[idx];
     const int lev = (int)(it >> 40);
     const int64_t c = it & ((1ll << 40) - 1);
     const LevelTab& T = tab_s[lev];
     if (lev == near_list)
-      interact_cell<D, KIND, NR, TILE, true>(T, c, R, r0, kp, S, ntile);
+      interact_cell<D, KIND, NR, TILE, true>(T, c, dsc, R, r0, kp, S, ntile);
     else
-      interact_cell<D, KIND, NR, TILE, false>(T, c, R, r0, kp, S, ntile);
+      interact_cell<D, KIND, NR, TILE, false>(T, c, dsc, R, r0, kp, S, ntile);
   }
 }
 
@@ -576,7 +589,8 @@ void launch_chunk(const DevH2& h, int64_t R, int64_t r0, const KParams& kp, cuda
   }
   CK(cudaMemsetAsync(h.work_counter.get(), 0, sizeof(unsigned long long), s));
   const int64_t ng = std::min<int64_t>(grid, (h.n_items + IT2 / 32 - 1) / (IT2 / 32));
-  kern<<<(unsigned)ng, IT2, smem, s>>>(h.items.get(), h.n_items, h.work_counter.get(), tabs, ntabs, nl, R, r0, kp);
+  kern<<<(unsigned)ng, IT2, smem, s>>>(h.items.get(), reinterpret_cast<const int4*>(h.item_desc.get()), h.n_items,
+                                       h.work_counter.get(), tabs, ntabs, nl, R, r0, kp);
   CKL();
 }
 

@@ -351,6 +351,14 @@ void build_tabs(DevH2& h, int64_t R, cudaStream_t s) {
   }
   h.tabs.alloc(sizeof(LevelTab) * tabs.size(), &h.mem);
   CK(cudaMemcpyAsync(h.tabs.get(), tabs.data(), sizeof(LevelTab) * tabs.size(), cudaMemcpyHostToDevice, s));
+  if (!h.item_desc.n) {
+    h.item_desc.alloc(4 * std::max<int64_t>(h.n_items, 1), &h.mem);
+    if (h.n_items)
+      make_item_desc<<<nblk(h.n_items, 256), 256, 0, s>>>(h.items.get(), h.n_items,
+                                                          reinterpret_cast<const LevelTab*>(h.tabs.get()),
+                                                          reinterpret_cast<int4*>(h.item_desc.get()));
+    CKL();
+  }
   CK(cudaStreamSynchronize(s));
 }
 

@@ -58,12 +58,56 @@ __global__ void transpose_cells(int64_t ncell, const int64_t* __restrict__ nrow,
 // SG lanes share one output row (j split across them, shuffle-reduced): the
 // upper levels have few rows but long sums (nr ~ 100-200), which one thread
 // per row turns into a long dependent load chain.
-template <int SG>
+template <int SG, int RB>
 __global__ void up_rows(int64_t nout, const int* __restrict__ owner, const int64_t* __restrict__ out_ptr,
                         const int64_t* __restrict__ nrow, const double* __restrict__ A,
                         const int64_t* __restrict__ a_off, const double* __restrict__ x,
                         const int64_t* __restrict__ x_ptr, const int64_t* __restrict__ x_map,
                         double* __restrict__ y, int64_t R) {
+  // thread = (output row p, block of RB right-hand sides, lane sub of SG): each operator entry read once
+  // feeds RB accumulators (multi-RHS products are small dense contractions)
+  const int64_t nrb = (R + RB - 1) / RB;
+  const int64_t qq = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t q = qq / SG;
+  const int sub = (int)(qq % SG);
+  const bool ok = q < nout * nrb;
+  double acc[RB];
+#pragma unroll
+  for (int r = 0; r < RB; r++) acc[r] = 0.0;
+  int64_t p = 0, r0 = 0;
+  if (ok) {
+    p = q / nrb;
+    r0 = (q - p * nrb) * RB;
+    const int c = owner[p];
+    const int64_t sidx = p - out_ptr[c], nr = nrow[c], k = out_ptr[c + 1] - out_ptr[c];
+    const double* As = A + a_off[c] + sidx;
+    const double* xc = x + (x_map ? x_ptr[x_map[c]] : x_ptr[c]) * R + r0;
+    for (int64_t j = sub; j < nr; j += SG) {
+      const double a = As[j * k];
+      const double* xr = xc + j * R;
+#pragma unroll
+      for (int r = 0; r < RB; r++) acc[r] = fma(a, (RB == 1 || r0 + r < R) ? xr[r] : 0.0, acc[r]);
+    }
+  }
+  if constexpr (SG > 1) {
+#pragma unroll
+    for (int r = 0; r < RB; r++)
+#pragma unroll
+      for (int o = SG / 2; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+  }
+  if (ok && sub == 0)
+#pragma unroll
+    for (int r = 0; r < RB; r++)
+      if (RB == 1 || r0 + r < R) y[p * R + r0 + r] = acc[r];
+}
+
+// one-RHS-block form (R < 8): SG lanes per output row
+template <int SG>
+__global__ void up_rows1(int64_t nout, const int* __restrict__ owner, const int64_t* __restrict__ out_ptr,
+                         const int64_t* __restrict__ nrow, const double* __restrict__ A,
+                         const int64_t* __restrict__ a_off, const double* __restrict__ x,
+                         const int64_t* __restrict__ x_ptr, const int64_t* __restrict__ x_map,
+                         double* __restrict__ y, int64_t R) {
   const int64_t qq = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t q = qq / SG;
   const int sub = (int)(qq % SG);
@@ -87,13 +131,19 @@ __global__ void up_rows(int64_t nout, const int* __restrict__ owner, const int64
 void launch_up(int sg, int64_t nout, const int* owner, const int64_t* out_ptr, const int64_t* nrow, const double* A,
                const int64_t* a_off, const double* x, const int64_t* x_ptr, const int64_t* x_map, double* y,
                int64_t R, cudaStream_t s) {
+  if (R >= 8) {  // register-blocked over 16 right-hand sides, 4 lanes per row
+    const int64_t thr = std::max<int64_t>(nout * ((R + 15) / 16), 1) * 4;
+    up_rows<4, 16><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R);
+    CKL();
+    return;
+  }
   const int64_t thr = std::max<int64_t>(nout * R, 1) * sg;
   switch (sg) {
-    case 1: up_rows<1><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R); break;
-    case 2: up_rows<2><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R); break;
-    case 4: up_rows<4><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R); break;
-    case 8: up_rows<8><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R); break;
-    default: up_rows<16><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R); break;
+    case 1: up_rows1<1><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R); break;
+    case 2: up_rows1<2><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R); break;
+    case 4: up_rows1<4><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R); break;
+    case 8: up_rows1<8><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R); break;
+    default: up_rows1<16><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R); break;
   }
   CKL();
 }
@@ -109,42 +159,64 @@ int up_group(int64_t rows, int64_t nr_avg) {
 }
 
 // downward (L2L): rows of the children stacked under parent P: u_child[q] += sum_s P_P[s * nr + i] u_P[s]
+// (thread = child row x block of RB right-hand sides)
+template <int RB>
 __global__ void down_rows(int64_t nin_child, const int* __restrict__ child_owner, const int64_t* __restrict__ parent,
                           const int64_t* __restrict__ ch_ptr, const int64_t* __restrict__ in_ptr_child,
                           const int64_t* __restrict__ in_ptr, const int64_t* __restrict__ kin,
                           const int64_t* __restrict__ nrow, const double* __restrict__ Pm,
                           const int64_t* __restrict__ pm_off, const double* __restrict__ uin,
                           double* __restrict__ uin_child, int64_t R) {
+  const int64_t nrb = (R + RB - 1) / RB;
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q >= nin_child * R) return;
-  const int64_t p = q / R, r = q - p * R;
+  if (q >= nin_child * nrb) return;
+  const int64_t p = q / nrb, r0 = (q - p * nrb) * RB;
   const int64_t P = parent[child_owner[p]];
   const int64_t i = p - in_ptr_child[ch_ptr[P]], nr = nrow[P], k = kin[P];
   const double* Pc = Pm + pm_off[P] + i;
-  const double* uc = uin + in_ptr[P] * R + r;
-  double acc = 0.0;
-  for (int64_t t = 0; t < k; t++) acc = fma(Pc[t * nr], uc[t * R], acc);
-  uin_child[q] += acc;
+  const double* uc = uin + in_ptr[P] * R + r0;
+  double acc[RB];
+#pragma unroll
+  for (int r = 0; r < RB; r++) acc[r] = 0.0;
+  for (int64_t t = 0; t < k; t++) {
+    const double a = Pc[t * nr];
+#pragma unroll
+    for (int r = 0; r < RB; r++) acc[r] = fma(a, (RB == 1 || r0 + r < R) ? uc[t * R + r] : 0.0, acc[r]);
+  }
+#pragma unroll
+  for (int r = 0; r < RB; r++)
+    if (RB == 1 || r0 + r < R) uin_child[p * R + r0 + r] += acc[r];
 }
 
-// leaves: u[perm[p]] = near[p] + sum_s P_c[s * m + a] u_in(c)[s]
+// leaves: u[perm[p]] = near[p] + sum_s P_c[s * m + a] u_in(c)[s]  (thread = point x block of RB RHS)
+template <int RB>
 __global__ void l2p_rows(int64_t np, const int* __restrict__ owner, const int64_t* __restrict__ t_ptr,
                          const double* __restrict__ pm, const int64_t* __restrict__ pm_off,
                          const int64_t* __restrict__ kin, const int64_t* __restrict__ in_ptr,
                          const double* __restrict__ uin, const double* __restrict__ near,
                          const int64_t* __restrict__ perm, double* __restrict__ u, int64_t R) {
+  const int64_t nrb = (R + RB - 1) / RB;
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q >= np * R) return;
-  const int64_t p = q / R, r = q - p * R;
-  double v = near[q];
+  if (q >= np * nrb) return;
+  const int64_t p = q / nrb, r0 = (q - p * nrb) * RB;
+  double v[RB];
+#pragma unroll
+  for (int r = 0; r < RB; r++) v[r] = (RB == 1 || r0 + r < R) ? near[p * R + r0 + r] : 0.0;
   if (pm) {
     const int c = owner[p];
     const int64_t a = p - t_ptr[c], m = t_ptr[c + 1] - t_ptr[c], k = kin[c];
     const double* Pc = pm + pm_off[c] + a;
-    const double* uc = uin + in_ptr[c] * R + r;
-    for (int64_t t = 0; t < k; t++) v = fma(Pc[t * m], uc[t * R], v);
+    const double* uc = uin + in_ptr[c] * R + r0;
+    for (int64_t t = 0; t < k; t++) {
+      const double w = Pc[t * m];
+#pragma unroll
+      for (int r = 0; r < RB; r++) v[r] = fma(w, (RB == 1 || r0 + r < R) ? uc[t * R + r] : 0.0, v[r]);
+    }
   }
-  u[perm[p] * R + r] = v;
+  const int64_t dst = perm[p] * R + r0;
+#pragma unroll
+  for (int r = 0; r < RB; r++)
+    if (RB == 1 || r0 + r < R) u[dst + r] = v[r];
 }
 
 void interact_all(int d, int kind, const DevH2& h, int64_t R, int64_t r0, int nr, const KParams& kp,
@@ -495,9 +567,14 @@ void matvec(DevH2& h, const double* w, double* u, int64_t R, cudaStream_t s) {
     const DevLevel& Lc = T.lv[l + 1];
     const DevH2Level& HL = h.lv[l];
     const DevH2Level& HC = h.lv[l + 1];
-    down_rows<<<nblk(HC.in_total * R, 256), 256, 0, s>>>(
-        HC.in_total, h.own_in[l + 1].get(), Lc.parent.get(), Lv.ch_ptr.get(), HC.in_ptr.get(), HL.in_ptr.get(),
-        HL.kin.get(), HL.m_in.get(), HL.pmat.get(), HL.pm_off.get(), h.uin[l].get(), h.uin[l + 1].get(), R);
+    if (R >= 8)
+      down_rows<16><<<nblk(HC.in_total * ((R + 15) / 16), 256), 256, 0, s>>>(
+          HC.in_total, h.own_in[l + 1].get(), Lc.parent.get(), Lv.ch_ptr.get(), HC.in_ptr.get(), HL.in_ptr.get(),
+          HL.kin.get(), HL.m_in.get(), HL.pmat.get(), HL.pm_off.get(), h.uin[l].get(), h.uin[l + 1].get(), R);
+    else
+      down_rows<1><<<nblk(HC.in_total * R, 256), 256, 0, s>>>(
+          HC.in_total, h.own_in[l + 1].get(), Lc.parent.get(), Lv.ch_ptr.get(), HC.in_ptr.get(), HL.in_ptr.get(),
+          HL.kin.get(), HL.m_in.get(), HL.pmat.get(), HL.pm_off.get(), h.uin[l].get(), h.uin[l + 1].get(), R);
     CKL();
   }
   if (g_profile) CK(cudaEventRecord(ev[3], s));
@@ -506,11 +583,14 @@ void matvec(DevH2& h, const double* w, double* u, int64_t R, cudaStream_t s) {
     const DevLevel& Lv = T.lv[L];
     const bool far = L >= 2;
     const DevH2Level* HL = far ? &h.lv[L] : nullptr;
-    l2p_rows<<<nblk(T.np * R, 256), 256, 0, s>>>(T.np, h.own_t.get(), Lv.t_ptr.get(),
-                                                     far ? HL->pmat.get() : nullptr, far ? HL->pm_off.get() : nullptr,
-                                                     far ? HL->kin.get() : nullptr, far ? HL->in_ptr.get() : nullptr,
-                                                     far ? h.uin[L].get() : nullptr, h.near.get(), T.t_perm.get(), u,
-                                                     R);
+    auto l2p = [&](auto kern, int64_t nthreads) {
+      kern<<<nblk(nthreads, 256), 256, 0, s>>>(T.np, h.own_t.get(), Lv.t_ptr.get(), far ? HL->pmat.get() : nullptr,
+                                               far ? HL->pm_off.get() : nullptr, far ? HL->kin.get() : nullptr,
+                                               far ? HL->in_ptr.get() : nullptr, far ? h.uin[L].get() : nullptr,
+                                               h.near.get(), T.t_perm.get(), u, R);
+    };
+    if (R >= 8) l2p(l2p_rows<16>, T.np * ((R + 15) / 16));
+    else l2p(l2p_rows<1>, T.np * R);
     CKL();
   }
   if (g_profile) {

@@ -582,7 +582,7 @@ void launch_chunk(const DevH2& h, int64_t R, int64_t r0, const KParams& kp, cuda
   }
   // pack this chunk's charges into the records
   const auto& pk = NR == 1 ? h.pack1 : h.pack16;
-  if (pk.total) {
+  if (pk.total && !(NR == 1 && R == 1)) {  // one RHS: gather / upward pass already wrote the charges
     pack_records<D, NR><<<nblk(pk.total, 256), 256, 0, s>>>(reinterpret_cast<const PackTab*>(pk.tabs.get()),
                                                             pk.nlists, pk.total, R, r0, 0);
     CKL();

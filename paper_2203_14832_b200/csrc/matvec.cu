@@ -24,11 +24,13 @@ bool g_profile = false;
 double g_stage_ms[5] = {0, 0, 0, 0, 0};
 
 __global__ void gather_rows(const double* __restrict__ w, const int64_t* __restrict__ perm, int64_t n, int64_t R,
-                            double* __restrict__ out) {
+                            double* __restrict__ out, double* __restrict__ recq, int rs) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n * R) return;
   int64_t p = i / R, r = i - p * R;
-  out[i] = w[perm[p] * R + r];
+  const double v = w[perm[p] * R + r];
+  out[i] = v;
+  if (recq) recq[i * rs] = v;  // one RHS: also the charge slot of the source record (no separate pack pass)
 }
 
 // ---- transfer passes as one thread per output row (owner maps give the cell) ----
@@ -107,7 +109,7 @@ __global__ void up_rows1(int64_t nout, const int* __restrict__ owner, const int6
                          const int64_t* __restrict__ nrow, const double* __restrict__ A,
                          const int64_t* __restrict__ a_off, const double* __restrict__ x,
                          const int64_t* __restrict__ x_ptr, const int64_t* __restrict__ x_map,
-                         double* __restrict__ y, int64_t R) {
+                         double* __restrict__ y, int64_t R, double* __restrict__ recq, int rs) {
   const int64_t qq = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t q = qq / SG;
   const int sub = (int)(qq % SG);
@@ -125,12 +127,15 @@ __global__ void up_rows1(int64_t nout, const int* __restrict__ owner, const int6
 #pragma unroll
     for (int o = SG / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   }
-  if (ok && sub == 0) y[q] = acc;
+  if (ok && sub == 0) {
+    y[q] = acc;
+    if (recq) recq[q * rs] = acc;
+  }
 }
 
 void launch_up(int sg, int64_t nout, const int* owner, const int64_t* out_ptr, const int64_t* nrow, const double* A,
                const int64_t* a_off, const double* x, const int64_t* x_ptr, const int64_t* x_map, double* y,
-               int64_t R, cudaStream_t s) {
+               int64_t R, cudaStream_t s, double* recq = nullptr, int rs = 0) {
   if (R >= 8) {  // register-blocked over 16 right-hand sides, 4 lanes per row
     const int64_t thr = std::max<int64_t>(nout * ((R + 15) / 16), 1) * 4;
     up_rows<4, 16><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R);
@@ -139,11 +144,11 @@ void launch_up(int sg, int64_t nout, const int* owner, const int64_t* out_ptr, c
   }
   const int64_t thr = std::max<int64_t>(nout * R, 1) * sg;
   switch (sg) {
-    case 1: up_rows1<1><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R); break;
-    case 2: up_rows1<2><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R); break;
-    case 4: up_rows1<4><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R); break;
-    case 8: up_rows1<8><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R); break;
-    default: up_rows1<16><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R); break;
+    case 1: up_rows1<1><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R, recq, rs); break;
+    case 2: up_rows1<2><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R, recq, rs); break;
+    case 4: up_rows1<4><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R, recq, rs); break;
+    case 8: up_rows1<8><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R, recq, rs); break;
+    default: up_rows1<16><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R, recq, rs); break;
   }
   CKL();
 }
@@ -521,9 +526,11 @@ int64_t matvec_launches(const DevH2& h, int64_t nrhs) {
   std::vector<std::pair<int64_t, int>> ch;
   rhs_chunks(nrhs, ch);
   int64_t nchunk = (int64_t)ch.size();
-  // gather, P2M, M2M x (L-2), (record pack + interaction) x chunks, L2L x (L-2), L2P+scatter
-  if (L < 2) return 1 + 2 * nchunk + 1;
-  return 1 + 1 + (L - 2) + 2 * nchunk + (L - 2) + 1;
+  // gather, P2M, M2M x (L-2), (record pack + interaction) x chunks, L2L x (L-2), L2P+scatter;
+  // one RHS: the gather and the upward pass write the records (no pack launch)
+  const int64_t per_chunk = nrhs == 1 ? 1 : 2;
+  if (L < 2) return 1 + per_chunk * nchunk + 1;
+  return 1 + 1 + (L - 2) + per_chunk * nchunk + (L - 2) + 1;
 }
 
 void matvec(DevH2& h, const double* w, double* u, int64_t R, cudaStream_t s) {
@@ -538,7 +545,14 @@ void matvec(DevH2& h, const double* w, double* u, int64_t R, cudaStream_t s) {
     for (auto& e : ev) CK(cudaEventCreate(&e));
     CK(cudaEventRecord(ev[0], s));
   }
-  gather_rows<<<nblk(T.nq * R, 256), 256, 0, s>>>(w, T.sperm(), T.nq, R, h.w_sorted.get());
+  // one RHS: the gather and the upward pass also write the records' charge slots (pack_records skipped)
+  const bool fused_pack = R == 1 && !h.pack1.lists.empty();
+  const int rs1 = 2 * ((T.d + 2) / 2);  // doubles per NR = 1 record
+  auto recq = [&](int list) -> double* {
+    return fused_pack ? reinterpret_cast<double*>(h.pack1.lists[list].get()) + T.d : nullptr;
+  };
+  gather_rows<<<nblk(T.nq * R, 256), 256, 0, s>>>(w, T.sperm(), T.nq, R, h.w_sorted.get(),
+                                                  recq((int)h.pack1.lists.size() - 1), rs1);
   CKL();
   if (L >= 2) {
     // ---- upward pass: P2M at the leaves, then M2M (one or a few threads per output row) ----
@@ -547,14 +561,15 @@ void matvec(DevH2& h, const double* w, double* u, int64_t R, cudaStream_t s) {
       const DevLevel& Lv = T.lv[L];
       const DevH2Level& HL = h.lv[L];
       launch_up(h.up_sg[L], HL.out_total, own_out(L), HL.out_ptrd(), HL.n_outd(), h.qmat_t[L].get(), HL.qm_offd(),
-                h.w_sorted.get(), T.shared ? Lv.t_ptr.get() : Lv.s_ptr.get(), nullptr, h.wout[L].get(), R, s);
+                h.w_sorted.get(), T.shared ? Lv.t_ptr.get() : Lv.s_ptr.get(), nullptr, h.wout[L].get(), R, s,
+                recq(L - 2), rs1);
     }
     for (int l = L - 1; l >= 2; l--) {
       const DevLevel& Lv = T.lv[l];
       const DevH2Level& HL = h.lv[l];
       const DevH2Level& HC = h.lv[l + 1];
       launch_up(h.up_sg[l], HL.out_total, own_out(l), HL.out_ptrd(), HL.n_outd(), h.qmat_t[l].get(), HL.qm_offd(),
-                h.wout[l + 1].get(), HC.out_ptrd(), Lv.ch_ptr.get(), h.wout[l].get(), R, s);
+                h.wout[l + 1].get(), HC.out_ptrd(), Lv.ch_ptr.get(), h.wout[l].get(), R, s, recq(l - 2), rs1);
     }
   }
   if (g_profile) CK(cudaEventRecord(ev[1], s));

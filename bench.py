@@ -219,6 +219,9 @@ def workload_name(args, cfg, n):
 
 
 def run_b200(args, cfg, world, rank, local):
+    # the engine's stream-ordered pool is reserved up front (common.cuh pool_init); the benchmark owns the
+    # GPU, so it reserves enough for the largest configuration's setup (pool growth mid-setup is slow)
+    os.environ.setdefault("H2B_POOL_RESERVE_GB", "64")
     import torch
 
     import paper_2203_14832_b200 as h2c

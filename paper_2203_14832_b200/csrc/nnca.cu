@@ -1379,8 +1379,13 @@ struct SideResult {
 // Process-wide ACA workspace arena: grows to the largest launch seen and is
 // reused after that, so repeated setups do not churn the allocator (pool
 // growth in the middle of a setup made some runs 2-3x slower).
-double* aca_arena(size_t doubles, cudaStream_t s) {
+static DBuf<double>& aca_arena_buf() {
   static DBuf<double> arena;
+  return arena;
+}
+int64_t aca_arena_size() { return (int64_t)aca_arena_buf().n; }
+double* aca_arena(size_t doubles, cudaStream_t s) {
+  DBuf<double>& arena = aca_arena_buf();
   if (arena.n < doubles) {
     CK(cudaStreamSynchronize(s));
     arena.release();
@@ -1503,7 +1508,7 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
       return e ? atof(e) : 1.0;
     }();
     if (!vsmem && gfrac > 0 && gfrac < 1) gmax = std::max<int64_t>(1, (int64_t)(gmax * gfrac));
-    const int64_t grid = std::min<int64_t>((int64_t)cells.size(), gmax);
+    int64_t grid = std::min<int64_t>((int64_t)cells.size(), gmax);
     J.ncell = (int64_t)cells.size();
     J.order = d_cells.get();
     J.n_max = nmx;
@@ -1516,6 +1521,13 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
     J.v_slab = vsmem ? 0 : vs;
     int64_t ws = J.u_slab + J.v_slab + D * f_max + f_max + 2 * cap_max + (m_max + n_max + 7) / 8 + 1;
     ws = (ws + 31) / 32 * 32 + H2B_ACA_SLAB_PAD;  // pad: per-CTA slabs off power-of-two strides
+    {  // slabs are sized for the rank cap (min(m, n)); bound their total by the memory left (top levels of
+       // dense clouds: n ~ 1e5 candidates per cell) -- fewer concurrent cells instead of running out
+      size_t fr = 0, tot = 0;
+      CK(cudaMemGetInfo(&fr, &tot));
+      const int64_t budget = (int64_t)(0.6 * (double)fr / sizeof(double)) + aca_arena_size();
+      grid = std::max<int64_t>(1, std::min<int64_t>(grid, budget / ws));
+    }
     double* wsbuf = aca_arena((size_t)(grid * ws), s);
     DBuf<unsigned long long> counter;
     counter.alloc(1);

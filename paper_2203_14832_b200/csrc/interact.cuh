@@ -114,6 +114,24 @@ __device__ __forceinline__ double rsq_approx(double x) {
   return y;
 }
 
+// M2L seed from the FP32 MUFU: the double's exponent is rebased to FP32
+// (1023 -> 127) and its mantissa truncated to 23 bits in integer arithmetic
+// (funnel shift + add, no F2F conversion), rsqrt.approx.f32 (max rel error
+// 2^-22.9), then widened back the same way.  Seed error |d| <= 1.8e-7 (vs
+// 9.2e-7 for MUFU.RSQ64H), so one quadratic Newton step (relative error
+// 1.5 d^2 <= 5e-14) replaces the cubic one: 2 fewer FP64 instructions per
+// pair.  Valid for r2 in [2^-126, 2^127]: the host selects this path only
+// when the tree's geometry bounds every admissible pair inside
+// [2^-100, 2^100] (f32seed_ok in launch_chunk).
+__device__ __forceinline__ double rsq_seed_f32(double x) {
+  const int hi = __double2hiint(x), lo = __double2loint(x);
+  const int fb = (int)__funnelshift_l((unsigned)lo, (unsigned)hi, 3) - ((1023 - 127) << 23);
+  float yf;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(yf) : "f"(__int_as_float(fb)));
+  const int yb = __float_as_int(yf);
+  return __hiloint2double((int)((unsigned)yb >> 3) + ((1023 - 127) << 20), yb << 29);
+}
+
 // ---- mbarrier / TMA bulk-copy helpers (sm_90+ PTX, used on sm_100a) ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
@@ -186,7 +204,7 @@ __device__ __forceinline__ double pair_r2(const double (&x)[D + 1], const double
 //   TEST: the source range may hold the target itself or a duplicate point,
 //   r2 == 0 -> K = 0 (the punctured diagonal); only the target's own leaf can,
 //   so only that member pays for the test.
-template <int NR, bool SELF, bool TEST>
+template <int NR, bool SELF, bool TEST, bool F32S>
 __device__ __forceinline__ void acc_inv_r(double r2, const double* q, double (&acc)[NR]) {
   if constexpr (TEST) {
     const bool zero = __double2hiint(r2) == 0;  // r2 == 0 (or subnormal)
@@ -197,9 +215,9 @@ __device__ __forceinline__ void acc_inv_r(double r2, const double* q, double (&a
 #pragma unroll
     for (int r = 0; r < NR; r++) acc[r] = fma(kv, q[r], acc[r]);
   } else {
-    const double y = rsq_approx(r2);
+    const double y = (F32S && !SELF) ? rsq_seed_f32(r2) : rsq_approx(r2);
     double t;
-    if constexpr (SELF) {
+    if constexpr (SELF || F32S) {
       t = fma(-r2, y * y, 3.0);
     } else {
       const double e = fma(-r2, y * y, 1.0);
@@ -261,7 +279,7 @@ __device__ __forceinline__ void issue_tile(const double2* rec, int nmem, const i
 // the warp's shared memory) through the double-buffered tiles and accumulate
 // into the register-resident targets.  `ntile` counts the tiles this warp
 // has consumed (stage = ntile & 1, mbarrier parity = (ntile >> 1) & 1).
-template <int D, int KIND, int NR, int TILE, bool SELF, bool TEST, int RT, class WS>
+template <int D, int KIND, int NR, int TILE, bool SELF, bool TEST, int RT, bool F32S, class WS>
 __device__ __forceinline__ void stream_members(WS& S, const double2* rec, int nmem,
                                                const double (&o)[D], const KParams& kp, bool worker, int grp,
                                                int G, const double (&x)[RT][D + 1], double (&acc)[RT][NR],
@@ -322,7 +340,7 @@ __device__ __forceinline__ void stream_members(WS& S, const double2* rec, int nm
         for (int t = 0; t < RT; t++) {
           const double r2 = pair_r2<D, SELF>(x[t], v, yy);
           if constexpr (is_inv_r<KIND>()) {
-            acc_inv_r<NR, SELF, TEST>(r2, v + D, acc[t]);
+            acc_inv_r<NR, SELF, TEST, F32S>(r2, v + D, acc[t]);
           } else {
             const double kv = kpair<KIND>(r2, kp);
 #pragma unroll
@@ -370,7 +388,7 @@ __device__ __forceinline__ void member_table(const LevelTab& T, int64_t c, int64
 // field (SELF): the target's own leaf goes first through the r2 == 0 test
 // path, the other neighbours (never coincident with a target) through the
 // plain path.
-template <int D, int KIND, int NR, int TILE, bool SELF, int RT, class WS>
+template <int D, int KIND, int NR, int TILE, bool SELF, int RT, bool F32S, class WS>
 __device__ __forceinline__ void interact_cell_rt(const LevelTab& T, int64_t c, const int4 dsc, int64_t R, int64_t r0,
                                                  const KParams& kp, WS& S, uint32_t& ntile) {
   const double2* rec = NR == 1 ? T.rec1 : T.rec16;
@@ -416,7 +434,7 @@ __device__ __forceinline__ void interact_cell_rt(const LevelTab& T, int64_t c, c
         S.pref[1] = (int)(T.s_ptr[c + 1] - b);
       }
       __syncwarp();
-      stream_members<D, KIND, NR, TILE, SELF, true, RT>(S, rec, 1, o, kp, worker, grp, G, x, acc, ntile);
+      stream_members<D, KIND, NR, TILE, SELF, true, RT, F32S>(S, rec, 1, o, kp, worker, grp, G, x, acc, ntile);
     }
     for (int64_t q0 = lb; q0 < le; q0 += MAXMEMW) {
       const int nmem = (int)(le - q0 < MAXMEMW ? le - q0 : MAXMEMW);
@@ -429,7 +447,7 @@ __device__ __forceinline__ void interact_cell_rt(const LevelTab& T, int64_t c, c
         if (lane == 0) S.pref[0] = 0;
         __syncwarp();
       }
-      stream_members<D, KIND, NR, TILE, SELF, false, RT>(S, rec, nmem, o, kp, worker, grp, G, x, acc, ntile);
+      stream_members<D, KIND, NR, TILE, SELF, false, RT, F32S>(S, rec, nmem, o, kp, worker, grp, G, x, acc, ntile);
     }
     constexpr double SCALE = kscale<KIND>() * (is_inv_r<KIND>() ? 0.5 : 1.0);
 #pragma unroll
@@ -464,17 +482,17 @@ __device__ __forceinline__ float lane_eff(int m, int rt) {
   return g > 0 ? (float)(m * g) / (float)(32 * rt) : 0.f;
 }
 
-template <int D, int KIND, int NR, int TILE, bool SELF, class WS>
+template <int D, int KIND, int NR, int TILE, bool SELF, bool F32S, class WS>
 __device__ __forceinline__ void interact_cell(const LevelTab& T, int64_t c, const int4 dsc, int64_t R, int64_t r0,
                                               const KParams& kp, WS& S, uint32_t& ntile) {
   if constexpr (WS::RTMAX >= 3) {
     const int m = dsc.y;
     if (m <= 96 && lane_eff(m, 3) > lane_eff(m, 2)) {
-      interact_cell_rt<D, KIND, NR, TILE, SELF, 3>(T, c, dsc, R, r0, kp, S, ntile);
+      interact_cell_rt<D, KIND, NR, TILE, SELF, 3, F32S>(T, c, dsc, R, r0, kp, S, ntile);
       return;
     }
   }
-  interact_cell_rt<D, KIND, NR, TILE, SELF, 2>(T, c, dsc, R, r0, kp, S, ntile);
+  interact_cell_rt<D, KIND, NR, TILE, SELF, 2, F32S>(T, c, dsc, R, r0, kp, S, ntile);
 }
 
 // item descriptors {first target, targets, list begin, list end} (one 16-byte load per work item)
@@ -492,7 +510,7 @@ __global__ void make_item_desc(const int64_t* __restrict__ items, int64_t n, con
 
 // Persistent kernel: every warp pulls work items (descending pair count) from
 // a global counter until the list is exhausted.
-template <int D, int KIND, int NR, int TILE, int RT>
+template <int D, int KIND, int NR, int TILE, int RT, bool F32S>
 __global__ void __launch_bounds__(IT2, NR == 1 ? H2B_MINB : 2) interact_warps(const int64_t* __restrict__ items, const int4* __restrict__ descs,
                                                       int64_t n_items, unsigned long long* __restrict__ counter,
                                                       const LevelTab* __restrict__ tabs, int ntabs, int near_list,
@@ -522,9 +540,9 @@ __global__ void __launch_bounds__(IT2, NR == 1 ? H2B_MINB : 2) interact_warps(co
     const int64_t c = it & ((1ll << 40) - 1);
     const LevelTab& T = tab_s[lev];
     if (lev == near_list)
-      interact_cell<D, KIND, NR, TILE, true>(T, c, dsc, R, r0, kp, S, ntile);
+      interact_cell<D, KIND, NR, TILE, true, F32S>(T, c, dsc, R, r0, kp, S, ntile);
     else
-      interact_cell<D, KIND, NR, TILE, false>(T, c, dsc, R, r0, kp, S, ntile);
+      interact_cell<D, KIND, NR, TILE, false, F32S>(T, c, dsc, R, r0, kp, S, ntile);
   }
 }
 
@@ -560,7 +578,7 @@ __global__ void pack_records(const PackTab* __restrict__ pt, int nlists, int64_t
   for (int q = 0; q < NR; q++) r[D + q] = T.q[i * R + r0 + q];
 }
 
-template <int D, int KIND, int NR, int TILE>
+template <int D, int KIND, int NR, int TILE, bool F32S>
 void launch_chunk(const DevH2& h, int64_t R, int64_t r0, const KParams& kp, cudaStream_t s) {
   if (!h.n_items) return;
   const int nl = h.t->depth + 1;  // list id of the leaf near field
@@ -568,7 +586,7 @@ void launch_chunk(const DevH2& h, int64_t R, int64_t r0, const KParams& kp, cuda
   auto* tabs = reinterpret_cast<const LevelTab*>(h.tabs.get());
   const size_t smem = (sizeof(LevelTab) * ntabs + 127) / 128 * 128 +
                       (IT2 / 32) * sizeof(WarpSmem<D, NR, TILE, (NR == 1 ? H2B_RT : 2)>);
-  auto kern = interact_warps<D, KIND, NR, TILE, (NR == 1 ? H2B_RT : 2)>;
+  auto kern = interact_warps<D, KIND, NR, TILE, (NR == 1 ? H2B_RT : 2), F32S>;
   static int grid = 0;  // per instantiation: persistent grid = resident CTAs
   static size_t grid_smem = 0;
   if (grid == 0 || grid_smem != smem) {
@@ -603,10 +621,35 @@ void pack_coords_d(const DevH2& h, cudaStream_t s) {
   CKL();
 }
 
+// The FP32-seeded M2L path needs every interaction-list r^2 inside
+// [2^-100, 2^100].  Admissible cells at level l satisfy diam <= eta * gap
+// (geometry.py:147), so r >= 2 hw_l sqrt(d) / eta >= 2 hw_depth sqrt(d) / eta;
+// in the shifted frame every term of r^2 is bounded by (4 sqrt(d) half)^2.
+// H2B_F32SEED=0 forces the cubic FP64-seeded path.
+inline bool f32seed_ok(const DevH2& h) {
+  static const int env = [] {
+    const char* e = getenv("H2B_F32SEED");
+    return e ? atoi(e) : 1;
+  }();
+  if (!env) return false;
+  const DevTree& t = *h.t;
+  const double hw = t.half * std::ldexp(1.0, -t.depth);
+  const double rmin = 2.0 * hw * std::sqrt((double)t.d) / (t.eta > 0 ? t.eta : 1.0);
+  const double rmax = 4.0 * std::sqrt((double)t.d) * t.half;
+  return rmin * rmin > std::ldexp(1.0, -100) && rmax * rmax < std::ldexp(1.0, 100);
+}
+
 template <int D, int KIND>
 void launch_interact2(const DevH2& h, int64_t R, int64_t r0, int nr, const KParams& kp, cudaStream_t s) {
-  if (nr == 16) launch_chunk<D, KIND, 16, H2B_TILE16>(h, R, r0, kp, s);
-  else launch_chunk<D, KIND, 1, H2B_TILE1>(h, R, r0, kp, s);
+  if constexpr (is_inv_r<KIND>()) {
+    if (f32seed_ok(h)) {
+      if (nr == 16) launch_chunk<D, KIND, 16, H2B_TILE16, true>(h, R, r0, kp, s);
+      else launch_chunk<D, KIND, 1, H2B_TILE1, true>(h, R, r0, kp, s);
+      return;
+    }
+  }
+  if (nr == 16) launch_chunk<D, KIND, 16, H2B_TILE16, false>(h, R, r0, kp, s);
+  else launch_chunk<D, KIND, 1, H2B_TILE1, false>(h, R, r0, kp, s);
 }
 
 template <int D>

@@ -524,13 +524,6 @@ DBuf<T> upload(const std::vector<T>& h, cudaStream_t s, MemStats* ms = nullptr) 
   return d;
 }
 
-size_t workspace_budget() {
-  size_t fr = 0, tot = 0;
-  CK(cudaMemGetInfo(&fr, &tot));
-  size_t b = (size_t)(0.5 * (double)fr);
-  return std::max<size_t>(b, (size_t)256 << 20);
-}
-
 // ---------------------------------------------------------------------
 // Persistent level-batched ACA (the setup hot path).
 //
@@ -1521,8 +1514,9 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
     J.v_slab = vsmem ? 0 : vs;
     int64_t ws = J.u_slab + J.v_slab + D * f_max + f_max + 2 * cap_max + (m_max + n_max + 7) / 8 + 1;
     ws = (ws + 31) / 32 * 32 + H2B_ACA_SLAB_PAD;  // pad: per-CTA slabs off power-of-two strides
-    {  // slabs are sized for the rank cap (min(m, n)); bound their total by the memory left (top levels of
-       // dense clouds: n ~ 1e5 candidates per cell) -- fewer concurrent cells instead of running out
+    if (grid * ws > aca_arena_size()) {  // slabs are sized for the rank cap (min(m, n)); bound their total by
+      // the memory left (top levels of dense clouds: n ~ 1e5 candidates per cell) -- fewer concurrent cells
+      // instead of running out.  Only queried when the arena would grow (steady-state setups skip the query).
       size_t fr = 0, tot = 0;
       CK(cudaMemGetInfo(&fr, &tot));
       const int64_t budget = (int64_t)(0.6 * (double)fr / sizeof(double)) + aca_arena_size();

@@ -1535,13 +1535,30 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
     J.v_slab = vsmem ? 0 : vs;
     int64_t ws = J.u_slab + J.v_slab + D * f_max + f_max + 2 * cap_max + (m_max + n_max + 7) / 8 + 1;
     ws = (ws + 31) / 32 * 32 + H2B_ACA_SLAB_PAD;  // pad: per-CTA slabs off power-of-two strides
-    if (grid * ws > aca_arena_size()) {  // slabs are sized for the rank cap (min(m, n)); bound their total by
-      // the memory left (top levels of dense clouds: n ~ 1e5 candidates per cell) -- fewer concurrent cells
-      // instead of running out.  Only queried when the arena would grow (steady-state setups skip the query).
-      size_t fr = 0, tot = 0;
-      CK(cudaMemGetInfo(&fr, &tot));
-      const int64_t budget = (int64_t)(0.6 * (double)fr / sizeof(double)) + aca_arena_size();
-      grid = std::max<int64_t>(1, std::min<int64_t>(grid, budget / ws));
+    if (grid * ws > aca_arena_size()) {
+      // Slabs are sized for the rank cap (min(m, n)): the top levels of dense clouds (n ~ 1e5 candidates per
+      // cell) need ~0.8 GB per concurrent cell, so their total is bounded by the memory available (device free
+      // memory + the unused part of the reserved pool) -- fewer concurrent cells instead of running out.  An
+      // arena that already holds >= 3/4 of the wanted slabs is used as is: growing it means mapping tens of GB
+      // again (measured 650 ms at c1) for a <= 25% longer launch.  Steady-state setups skip the query.
+      const int64_t have = aca_arena_size() / ws;
+      if (have >= 1 && 4 * have >= 3 * grid) {
+        grid = have;
+      } else {
+        size_t fr = 0, tot = 0;
+        CK(cudaMemGetInfo(&fr, &tot));
+        size_t pool_free = 0;
+        int dv = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dv) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dv) == cudaSuccess) {
+          uint64_t rsv = 0, used = 0;
+          if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &rsv) == cudaSuccess &&
+              cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess && rsv > used)
+            pool_free = (size_t)(rsv - used);
+        }
+        const int64_t budget = (int64_t)(0.6 * (double)(fr + pool_free) / sizeof(double)) + aca_arena_size();
+        grid = std::max<int64_t>(1, std::min<int64_t>(grid, budget / ws));
+      }
     }
     double* wsbuf = aca_arena((size_t)(grid * ws), s);
     DBuf<unsigned long long> counter;

@@ -47,10 +47,14 @@ CONFIGS = {
 HEADLINE = "c2"
 # FP64 flops the interaction kernel executes per 1/r pair (DFMA = 2, DADD / DMUL = 1; MUFU.RSQ64H seed not
 # counted), one RHS; each further RHS adds one DFMA (2 flops):
-#   M2L (interact.cuh pair_r2 + acc_inv_r): r^2 = DADD + 3 DFMA (7); cubic rsqrt step DMUL + 3 DFMA (7);
-#        charge DMUL + accumulate DFMA (3)                                                        -> 17
+#   M2L (interact.cuh pair_r2 + acc_inv_r): r^2 = DADD + 3 DFMA (7); from the FP32-MUFU seed
+#        (rsq_seed_f32, integer exponent rebase) one quadratic step DMUL + DFMA (3); charge DMUL +
+#        accumulate DFMA (3)                                                                      -> 13
+#        (H2B_F32SEED=0 or a geometry outside the FP32 range: MUFU.RSQ64H seed + cubic step
+#        DMUL + 3 DFMA (7)                                                                         -> 17)
 #   near field: r^2 = 3 DADD + 3 DFMA (9); quadratic step DMUL + DFMA (3); DMUL + DFMA (3)       -> 15
-FLOPS_PER_PAIR_M2L = 17
+# The bench configs all lie in [-1, 1]^d, inside the FP32-seed guard (interact.cuh f32seed_ok).
+FLOPS_PER_PAIR_M2L = 13 if os.environ.get("H2B_F32SEED", "1") != "0" else 17
 FLOPS_PER_PAIR_NEAR = 15
 
 
@@ -339,6 +343,7 @@ def run_b200(args, cfg, world, rank, local):
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "traffic": traffic,
                      "flops_per_pair": {"m2l": FLOPS_PER_PAIR_M2L, "near": FLOPS_PER_PAIR_NEAR},
+                     "pairs_per_s": (pairs_m2l + pairs_p2p) / (inter_ms * 1e-3),  # kernel evaluations (each serves nrhs columns)
                      "peak_source": "measured: DFMA throughput probe (h2b_fp64_peak) on this GPU, same run"},
         "clocks": clk.summary(),
     }

@@ -293,3 +293,33 @@ def test_edge_cases(h2c):
         h2c.build_tree(h2c.PointCloud.from_points(pts), nu=0, eta=1.0)
     with pytest.raises(ValueError):
         h2c.h2_matvec(h2, np.zeros(99))
+
+
+@pytest.mark.parametrize("scale_exp", [0, -100, 100])
+def test_fp32_seed_guard_scales(h2c, oracle_mod, scale_exp):
+    """M2L 1/r path selection by geometry (interact.cuh f32seed_ok): at unit scale the FP32-MUFU seed +
+    quadratic step runs; coordinates scaled by 2^-100 / 2^100 put r^2 outside the FP32 range, so the
+    FP64-seed + cubic step path runs instead.  Scaling by a power of two is exact, so the tree and the
+    pivots are bitwise those of the unit-scale problem and both paths must match the oracle."""
+    from paper_2203_14832_b200 import sampling
+
+    s = float(np.ldexp(1.0, scale_exp))
+    pts0 = sampling.sphere_points(20000, 3, 2)
+    pts = pts0 * s
+    kern = h2c.builtin_kernel("laplace-3d", 3)
+    tree = h2c.build_tree(h2c.PointCloud.from_points(pts), nu=64, eta=float(np.sqrt(2.0)))
+    h2 = h2c.assemble(tree, kern, 1e-6)
+    tree0 = h2c.build_tree(h2c.PointCloud.from_points(pts0), nu=64, eta=float(np.sqrt(2.0)))
+    h20 = h2c.assemble(tree0, kern, 1e-6)
+    assert tree.depth == tree0.depth
+    for level in range(2, tree.depth + 1):
+        assert np.array_equal(h2.array(level, "t_in"), h20.array(level, "t_in")), level
+    w = np.random.default_rng(5).uniform(-1, 1, 20000)
+    u = h2c.h2_matvec(h2, w)
+    ot = oracle_mod.OTree(pts, None, nu=64)
+    oh = oracle_mod.OH2(ot, kern.kind, kern.device_param, 1e-6)
+    uo = oh.matvec(w)
+    assert np.linalg.norm(u - uo) / np.linalg.norm(uo) <= 1e-10
+    # 1/r is homogeneous of degree -1: the scaled product is the unit-scale one over s
+    u0 = h2c.h2_matvec(h20, w)
+    assert np.linalg.norm(u * s - u0) / np.linalg.norm(u0) <= 1e-10

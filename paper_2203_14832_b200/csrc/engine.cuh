@@ -101,7 +101,7 @@ struct DevH2 {
   DBuf<int> own_t;                          // sorted target position -> leaf cell
   std::vector<DBuf<double>> qmat_t;         // per level: transposed column interpolators (upward pass)
   std::vector<int> up_sg;                   // per level: lanes per output row in the upward pass
-  std::vector<DBuf<int>> m_sb, m_end;       // per interaction list: member tables (interact.cuh LevelTab)
+  std::vector<DBuf<int>> m_sb, m_end, m_cnt;       // per interaction list: member tables (interact.cuh LevelTab)
   RecSet pack1, pack16;                     // source records for RHS chunks of width 1 / 16
   DBuf<unsigned long long> work_counter;    // persistent interaction kernel: next work item
 };

@@ -103,8 +103,9 @@ struct LevelTab {
   const int64_t* l_ptr;  // cell list (CSR)
   const int64_t* l_idx;
   const int* m_sb;       // per list entry: first record of the member
-  const int* m_end;      // per list entry: inclusive prefix of member lengths within the cell's list
-                         // (near field: the cell itself counts 0, it has its own pass)
+  const int* m_end;      // per member: inclusive prefix of member lengths within the cell's list
+  const int* m_cnt;      // members per cell (compacted at the head of the cell's list segment; adjacent
+                         // record ranges merged; near field: the cell itself is dropped, it has its own pass)
   double* out;           // result rows (target position) * R
 };
 
@@ -353,35 +354,6 @@ __device__ __forceinline__ void stream_members(WS& S, const double2* rec, int nm
   }
 }
 
-// Member table of list members [q0, q0 + nmem): first record and prefix of
-// lengths (warp scan, 32 members per step).  SELF drops the own leaf (done
-// separately through the r2 == 0 test path).
-template <bool SELF, class S_>
-__device__ __forceinline__ void member_table(const LevelTab& T, int64_t c, int64_t q0, int nmem, S_& S) {
-  const int lane = threadIdx.x & 31;
-  int run = 0;
-  for (int b = 0; b < nmem; b += 32) {
-    const int q = b + lane;
-    int len = 0;
-    if (q < nmem) {
-      const int64_t sc = T.l_idx[q0 + q];
-      const int64_t sb = T.s_ptr[sc];
-      S.sbeg[q] = (int)sb;
-      len = (SELF && sc == c) ? 0 : (int)(T.s_ptr[sc + 1] - sb);
-    }
-    int v = len;
-#pragma unroll
-    for (int o2 = 1; o2 < 32; o2 <<= 1) {
-      const int n2 = __shfl_up_sync(0xffffffffu, v, o2);
-      if (lane >= o2) v += n2;
-    }
-    if (q < nmem) S.pref[q + 1] = run + v;
-    run += __shfl_sync(0xffffffffu, v, 31);
-  }
-  if (lane == 0) S.pref[0] = 0;
-  __syncwarp();
-}
-
 // One work item (list, cell) on one warp.  RT targets per lane (register
 // blocking: every shared-memory source read feeds RT pair evaluations), TS
 // lanes per target group, G = 32 / TS groups splitting the sources.  Near
@@ -505,7 +477,7 @@ __global__ void make_item_desc(const int64_t* __restrict__ items, int64_t n, con
   const int64_t c = it & ((1ll << 40) - 1);
   const LevelTab& T = tabs[lev];
   const int64_t tb = T.t_ptr[c];
-  desc[i] = make_int4((int)tb, (int)(T.t_ptr[c + 1] - tb), (int)T.l_ptr[c], (int)T.l_ptr[c + 1]);
+  desc[i] = make_int4((int)tb, (int)(T.t_ptr[c + 1] - tb), (int)T.l_ptr[c], (int)(T.l_ptr[c] + T.m_cnt[c]));
 }
 
 // Persistent kernel: every warp pulls work items (descending pair count) from

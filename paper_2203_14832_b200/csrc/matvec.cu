@@ -103,6 +103,14 @@ __global__ void up_rows(int64_t nout, const int* __restrict__ owner, const int64
       if (RB == 1 || r0 + r < R) y[p * R + r0 + r] = acc[r];
 }
 
+// Unroll of the P2M/M2M and L2P row loops (measured at the headline: no unrolling beats the compiler's
+// default and unroll 4 / 8 -- upward 0.287 -> 0.267 ms, L2P 0.074 -> 0.066 ms; the L2L loop keeps the default).
+#ifndef H2B_XU
+#define H2B_XU 1
+#endif
+#define H2B_PRAGMA_(x) _Pragma(#x)
+#define H2B_UNROLL_XU(n) H2B_PRAGMA_(unroll n)
+
 // one-RHS-block form (R < 8): SG lanes per output row
 template <int SG>
 __global__ void up_rows1(int64_t nout, const int* __restrict__ owner, const int64_t* __restrict__ out_ptr,
@@ -121,6 +129,7 @@ __global__ void up_rows1(int64_t nout, const int* __restrict__ owner, const int6
     const int64_t sidx = p - out_ptr[c], nr = nrow[c], k = out_ptr[c + 1] - out_ptr[c];
     const double* As = A + a_off[c] + sidx;
     const double* xc = x + (x_map ? x_ptr[x_map[c]] : x_ptr[c]) * R + r;
+    H2B_UNROLL_XU(H2B_XU)
     for (int64_t j = sub; j < nr; j += SG) acc = fma(As[j * k], xc[j * R], acc);
   }
   if constexpr (SG > 1) {
@@ -212,6 +221,7 @@ __global__ void l2p_rows(int64_t np, const int* __restrict__ owner, const int64_
     const int64_t a = p - t_ptr[c], m = t_ptr[c + 1] - t_ptr[c], k = kin[c];
     const double* Pc = pm + pm_off[c] + a;
     const double* uc = uin + in_ptr[c] * R + r0;
+    H2B_UNROLL_XU(H2B_XU)
     for (int64_t t = 0; t < k; t++) {
       const double w = Pc[t * m];
 #pragma unroll
@@ -243,20 +253,35 @@ void pack_coords(int d, const DevH2& h, int nr, cudaStream_t s) {
   }
 }
 
-// per-entry member tables of every interaction list (record start, inclusive length prefix within the
-// cell's list); the near field's own leaf counts 0 (it is handled by the r2 == 0 pass)
+// member tables of every interaction list: record start and inclusive length prefix per member, written
+// compacted at the head of the cell's list segment, m_cnt[c] entries.  Members whose record ranges are
+// adjacent (Morton-consecutive nonempty cells, common among siblings) are merged into one entry, so the
+// interaction kernel issues one TMA bulk copy for the run (merge = 0 keeps one entry per list member).  The
+// near field's own leaf is dropped (it is handled by the r2 == 0 pass).
 __global__ void member_tables(int64_t n, const int64_t* __restrict__ l_ptr, const int64_t* __restrict__ l_idx,
-                              const int64_t* __restrict__ s_ptr, int self_zero, int* __restrict__ m_sb,
-                              int* __restrict__ m_end) {
+                              const int64_t* __restrict__ s_ptr, int self_zero, int merge, int* __restrict__ m_sb,
+                              int* __restrict__ m_end, int* __restrict__ m_cnt) {
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= n) return;
-  int run = 0;
-  for (int64_t q = l_ptr[c]; q < l_ptr[c + 1]; q++) {
+  const int64_t q0 = l_ptr[c];
+  int run = 0, cnt = 0;
+  int64_t last_end = -1;
+  for (int64_t q = q0; q < l_ptr[c + 1]; q++) {
     const int64_t y = l_idx[q];
-    m_sb[q] = (int)s_ptr[y];
-    run += (self_zero && y == c) ? 0 : (int)(s_ptr[y + 1] - s_ptr[y]);
-    m_end[q] = run;
+    if (self_zero && y == c) continue;
+    const int64_t b = s_ptr[y], e = s_ptr[y + 1];
+    if (e == b) continue;
+    run += (int)(e - b);
+    if (merge && cnt > 0 && b == last_end) {
+      m_end[q0 + cnt - 1] = run;
+    } else {
+      m_sb[q0 + cnt] = (int)b;
+      m_end[q0 + cnt] = run;
+      cnt++;
+    }
+    last_end = e;
   }
+  m_cnt[c] = cnt;
 }
 
 // pair counts per work item (the reference's entry counts for S and near blocks)
@@ -376,6 +401,11 @@ void build_tabs(DevH2& h, int64_t R, cudaStream_t s) {
   if (h.m_sb.empty()) {  // member tables (static per H2 matrix)
     h.m_sb.resize(L + 2);
     h.m_end.resize(L + 2);
+    h.m_cnt.resize(L + 2);
+    static const int merge = [] {
+      const char* e = getenv("H2B_MERGE_MEMBERS");
+      return e ? atoi(e) : 1;
+    }();
     std::vector<int> ids;
     for (int l = 2; l <= L; l++) ids.push_back(l);
     ids.push_back(L + 1);  // the near field (also when the tree has fewer than two levels)
@@ -385,11 +415,13 @@ void build_tabs(DevH2& h, int64_t R, cudaStream_t s) {
       const int64_t tot = nf ? Lv.nb_total : Lv.il_total;
       h.m_sb[l].alloc(std::max<int64_t>(tot, 1), &h.mem);
       h.m_end[l].alloc(std::max<int64_t>(tot, 1), &h.mem);
+      h.m_cnt[l].alloc(std::max<int64_t>(Lv.n, 1), &h.mem);
       const int64_t* sp = nf ? (T.shared ? Lv.t_ptr.get() : Lv.s_ptr.get()) : h.lv[l].out_ptrd();
       if (Lv.n)
         member_tables<<<nblk(Lv.n, 256), 256, 0, s>>>(Lv.n, nf ? Lv.nb_ptr.get() : Lv.il_ptr.get(),
                                                          nf ? Lv.nb_idx.get() : Lv.il_idx.get(), sp, nf ? 1 : 0,
-                                                         h.m_sb[l].get(), h.m_end[l].get());
+                                                         merge, h.m_sb[l].get(), h.m_end[l].get(),
+                                                         h.m_cnt[l].get());
       CKL();
     }
   }
@@ -410,6 +442,7 @@ void build_tabs(DevH2& h, int64_t R, cudaStream_t s) {
       t.l_idx = Lv.il_idx.get();
       t.m_sb = h.m_sb[l].get();
       t.m_end = h.m_end[l].get();
+      t.m_cnt = h.m_cnt[l].get();
       t.out = h.uin[l].get();
     } else if (l == L + 1) {
       const DevLevel& Lv = T.lv[L];
@@ -423,6 +456,7 @@ void build_tabs(DevH2& h, int64_t R, cudaStream_t s) {
       t.l_idx = Lv.nb_idx.get();
       t.m_sb = h.m_sb[L + 1].get();
       t.m_end = h.m_end[L + 1].get();
+      t.m_cnt = h.m_cnt[L + 1].get();
       t.out = h.near.get();
     }
   }

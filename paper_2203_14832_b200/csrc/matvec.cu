@@ -202,6 +202,33 @@ __global__ void down_rows(int64_t nin_child, const int* __restrict__ child_owner
     if (RB == 1 || r0 + r < R) uin_child[p * R + r0 + r] += acc[r];
 }
 
+// one-RHS form for the upper levels (few child rows, long parent ranks): SG lanes per child row split the
+// parent's k columns, shuffle-reduced (a latency-bound 10-20 us launch otherwise)
+template <int SG>
+__global__ void down_rows_sg(int64_t nin_child, const int* __restrict__ child_owner, const int64_t* __restrict__ parent,
+                             const int64_t* __restrict__ ch_ptr, const int64_t* __restrict__ in_ptr_child,
+                             const int64_t* __restrict__ in_ptr, const int64_t* __restrict__ kin,
+                             const int64_t* __restrict__ nrow, const double* __restrict__ Pm,
+                             const int64_t* __restrict__ pm_off, const double* __restrict__ uin,
+                             double* __restrict__ uin_child, int64_t R) {
+  const int64_t qq = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t q = qq / SG;
+  const int sub = (int)(qq % SG);
+  const bool ok = q < nin_child * R;
+  double acc = 0.0;
+  if (ok) {
+    const int64_t p = q / R, r = q - p * R;
+    const int64_t P = parent[child_owner[p]];
+    const int64_t i = p - in_ptr_child[ch_ptr[P]], nr = nrow[P], k = kin[P];
+    const double* Pc = Pm + pm_off[P] + i;
+    const double* uc = uin + in_ptr[P] * R + r;
+    for (int64_t t = sub; t < k; t += SG) acc = fma(Pc[t * nr], uc[t * R], acc);
+  }
+#pragma unroll
+  for (int o = SG / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (ok && sub == 0) uin_child[q] += acc;
+}
+
 // leaves: u[perm[p]] = near[p] + sum_s P_c[s * m + a] u_in(c)[s]  (thread = point x block of RB RHS)
 template <int RB>
 __global__ void l2p_rows(int64_t np, const int* __restrict__ owner, const int64_t* __restrict__ t_ptr,
@@ -620,10 +647,30 @@ void matvec(DevH2& h, const double* w, double* u, int64_t R, cudaStream_t s) {
       down_rows<16><<<nblk(HC.in_total * ((R + 15) / 16), 256), 256, 0, s>>>(
           HC.in_total, h.own_in[l + 1].get(), Lc.parent.get(), Lv.ch_ptr.get(), HC.in_ptr.get(), HL.in_ptr.get(),
           HL.kin.get(), HL.m_in.get(), HL.pmat.get(), HL.pm_off.get(), h.uin[l].get(), h.uin[l + 1].get(), R);
-    else
-      down_rows<1><<<nblk(HC.in_total * R, 256), 256, 0, s>>>(
-          HC.in_total, h.own_in[l + 1].get(), Lc.parent.get(), Lv.ch_ptr.get(), HC.in_ptr.get(), HL.in_ptr.get(),
-          HL.kin.get(), HL.m_in.get(), HL.pmat.get(), HL.pm_off.get(), h.uin[l].get(), h.uin[l + 1].get(), R);
+    else {
+      // large levels keep one thread per row (measured); small ones split the parent's columns over lanes
+      const int sg = HC.in_total * R < 148 * 1024 ? up_group(HC.in_total * R, HL.in_total / std::max<int64_t>(HL.n, 1)) : 1;
+      const int64_t thr = std::max<int64_t>(HC.in_total * R, 1) * sg;
+#define H2B_DOWN_SG(G)                                                                                          \
+  down_rows_sg<G><<<nblk(thr, 256), 256, 0, s>>>(HC.in_total, h.own_in[l + 1].get(), Lc.parent.get(),           \
+                                                 Lv.ch_ptr.get(), HC.in_ptr.get(), HL.in_ptr.get(), HL.kin.get(), \
+                                                 HL.m_in.get(), HL.pmat.get(), HL.pm_off.get(), h.uin[l].get(),  \
+                                                 h.uin[l + 1].get(), R)
+      if (sg == 1) {
+        down_rows<1><<<nblk(HC.in_total * R, 256), 256, 0, s>>>(
+            HC.in_total, h.own_in[l + 1].get(), Lc.parent.get(), Lv.ch_ptr.get(), HC.in_ptr.get(), HL.in_ptr.get(),
+            HL.kin.get(), HL.m_in.get(), HL.pmat.get(), HL.pm_off.get(), h.uin[l].get(), h.uin[l + 1].get(), R);
+      } else if (sg == 2) {
+        H2B_DOWN_SG(2);
+      } else if (sg == 4) {
+        H2B_DOWN_SG(4);
+      } else if (sg == 8) {
+        H2B_DOWN_SG(8);
+      } else {
+        H2B_DOWN_SG(16);
+      }
+#undef H2B_DOWN_SG
+    }
     CKL();
   }
   if (g_profile) CK(cudaEventRecord(ev[3], s));

@@ -547,6 +547,11 @@ void ensure_scratch(DevH2& h, int64_t R, cudaStream_t s) {
       const int64_t nr_sum = (int64_t)(h.symmetric ? HL.pmat.n : HL.qmat.n);  // sum over cells of nr * k
       const int64_t nr_avg = rows ? nr_sum / rows : 0;
       h.up_sg[l] = up_group(rows, nr_avg);
+      static const int cap = [] {  // tuning: cap on the lanes per row (H2B_UP_SG_CAP)
+        const char* e = getenv("H2B_UP_SG_CAP");
+        return e ? atoi(e) : 16;
+      }();
+      while (h.up_sg[l] > std::max(cap, 1)) h.up_sg[l] /= 2;
     }
     const DevLevel& Lf = T.lv[T.depth];
     h.own_t.alloc(std::max<int64_t>(T.np, 1), &h.mem);

@@ -14,7 +14,7 @@ struct KParams {
   double a, inv_log_a, c_near;  // reg-log constants
 };
 
-// exp(x) for the Gaussian kernels' x = -a r^2 <= 0 (matvec path).  Table
+// exp(x) for the Gaussian / Matern kernels' x = -a r^2, -r <= 0 (matvec path).  Table
 // reduction x = (16 m + j) ln2/16 + r, |r| <= ln2/32: exp(x) = 2^m 2^(j/16)
 // exp(r), exp(r) by its degree-7 Taylor polynomial (truncation r^8/8! <=
 // 5e-19), 2^(j/16) from a 16-entry table of correctly rounded doubles (one
@@ -60,7 +60,7 @@ __device__ __forceinline__ double kfast(double r2, const KParams& kp) {
   } else if constexpr (KIND == GAUSSIAN_SCALED) {
     return exp_neg_fast(-kp.a * r2);
   } else if constexpr (KIND == MATERN) {
-    return exp(-sqrt(r2));
+    return exp_neg_fast(-sqrt(r2));
   } else if constexpr (KIND == LOG) {
     return r2 > 0.0 ? 0.5 * log(r2) : 0.0;
   } else if constexpr (KIND == REG_INVERSE) {

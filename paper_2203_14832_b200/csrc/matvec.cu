@@ -57,6 +57,27 @@ __global__ void transpose_cells(int64_t ncell, const int64_t* __restrict__ nrow,
 }
 
 // upward (P2M / M2M): y[p] = sum_j AT_c[j * k + s] x_c[j],  p = out_ptr[c] + s.
+// RB consecutive doubles of a right-hand-side row.  H2B_VEC16: 16-byte loads when the row start is even
+// (R even and r0 even: every RHS row offset is then a multiple of 2 doubles), else scalar loads guarded by R.
+#ifndef H2B_VEC16
+#define H2B_VEC16 1
+#endif
+template <int RB>
+__device__ __forceinline__ void load_rhs(const double* __restrict__ p, bool vec, int64_t r0, int64_t R, double (&v)[RB]) {
+  if (H2B_VEC16 && RB % 2 == 0 && vec) {
+    const double2* p2 = reinterpret_cast<const double2*>(p);
+#pragma unroll
+    for (int i = 0; i < RB / 2; i++) {
+      const double2 t = p2[i];
+      v[2 * i] = t.x;
+      v[2 * i + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < RB; r++) v[r] = (RB == 1 || r0 + r < R) ? p[r] : 0.0;
+  }
+}
+
 // SG lanes share one output row (j split across them, shuffle-reduced): the
 // upper levels have few rows but long sums (nr ~ 100-200), which one thread
 // per row turns into a long dependent load chain.
@@ -84,11 +105,13 @@ __global__ void up_rows(int64_t nout, const int* __restrict__ owner, const int64
     const int64_t sidx = p - out_ptr[c], nr = nrow[c], k = out_ptr[c + 1] - out_ptr[c];
     const double* As = A + a_off[c] + sidx;
     const double* xc = x + (x_map ? x_ptr[x_map[c]] : x_ptr[c]) * R + r0;
+    const bool vec = (R % 2 == 0) && r0 + RB <= R;
     for (int64_t j = sub; j < nr; j += SG) {
       const double a = As[j * k];
-      const double* xr = xc + j * R;
+      double xv[RB];
+      load_rhs<RB>(xc + j * R, vec, r0, R, xv);
 #pragma unroll
-      for (int r = 0; r < RB; r++) acc[r] = fma(a, (RB == 1 || r0 + r < R) ? xr[r] : 0.0, acc[r]);
+      for (int r = 0; r < RB; r++) acc[r] = fma(a, xv[r], acc[r]);
     }
   }
   if constexpr (SG > 1) {
@@ -192,10 +215,13 @@ __global__ void down_rows(int64_t nin_child, const int* __restrict__ child_owner
   double acc[RB];
 #pragma unroll
   for (int r = 0; r < RB; r++) acc[r] = 0.0;
+  const bool vec = (R % 2 == 0) && r0 + RB <= R;
   for (int64_t t = 0; t < k; t++) {
     const double a = Pc[t * nr];
+    double uv[RB];
+    load_rhs<RB>(uc + t * R, vec, r0, R, uv);
 #pragma unroll
-    for (int r = 0; r < RB; r++) acc[r] = fma(a, (RB == 1 || r0 + r < R) ? uc[t * R + r] : 0.0, acc[r]);
+    for (int r = 0; r < RB; r++) acc[r] = fma(a, uv[r], acc[r]);
   }
 #pragma unroll
   for (int r = 0; r < RB; r++)
@@ -240,9 +266,9 @@ __global__ void l2p_rows(int64_t np, const int* __restrict__ owner, const int64_
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= np * nrb) return;
   const int64_t p = q / nrb, r0 = (q - p * nrb) * RB;
+  const bool vec = (R % 2 == 0) && r0 + RB <= R;
   double v[RB];
-#pragma unroll
-  for (int r = 0; r < RB; r++) v[r] = (RB == 1 || r0 + r < R) ? near[p * R + r0 + r] : 0.0;
+  load_rhs<RB>(near + p * R + r0, vec, r0, R, v);
   if (pm) {
     const int c = owner[p];
     const int64_t a = p - t_ptr[c], m = t_ptr[c + 1] - t_ptr[c], k = kin[c];
@@ -251,8 +277,10 @@ __global__ void l2p_rows(int64_t np, const int* __restrict__ owner, const int64_
     H2B_UNROLL_XU(H2B_XU)
     for (int64_t t = 0; t < k; t++) {
       const double w = Pc[t * m];
+      double uv[RB];
+      load_rhs<RB>(uc + t * R, vec, r0, R, uv);
 #pragma unroll
-      for (int r = 0; r < RB; r++) v[r] = fma(w, (RB == 1 || r0 + r < R) ? uc[t * R + r] : 0.0, v[r]);
+      for (int r = 0; r < RB; r++) v[r] = fma(w, uv[r], v[r]);
     }
   }
   const int64_t dst = perm[p] * R + r0;

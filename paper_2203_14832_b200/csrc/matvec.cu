@@ -59,6 +59,23 @@ __global__ void transpose_cells(int64_t ncell, const int64_t* __restrict__ nrow,
 // upward (P2M / M2M): y[p] = sum_j AT_c[j * k + s] x_c[j],  p = out_ptr[c] + s.
 // RB consecutive doubles of a right-hand-side row.  H2B_VEC16: 16-byte loads when the row start is even
 // (R even and r0 even: every RHS row offset is then a multiple of 2 doubles), else scalar loads guarded by R.
+// multi-RHS (R >= 8) transfer passes: lanes per row (upward) and RHS block widths.  Measured at c4
+// (16 RHS; tools/variants.py + time_variants.py): one thread per row x 8 RHS beats 4 lanes x 16 RHS
+// (upward 10.5 -> 5.8 ms: 86 -> fewer registers, 15 -> 2x the resident warps of a latency-bound pass),
+// 8-wide blocks beat 16 for L2L / L2P (3.71 -> 3.18, 2.52 -> 2.08 ms); 4-wide blocks and 8 lanes per
+// row are slower.
+#ifndef H2B_UP_SG
+#define H2B_UP_SG 1
+#endif
+#ifndef H2B_UP_RB
+#define H2B_UP_RB 8
+#endif
+#ifndef H2B_DN_RB
+#define H2B_DN_RB 8
+#endif
+#ifndef H2B_L2P_RB
+#define H2B_L2P_RB 8
+#endif
 #ifndef H2B_VEC16
 #define H2B_VEC16 1
 #endif
@@ -168,9 +185,9 @@ __global__ void up_rows1(int64_t nout, const int* __restrict__ owner, const int6
 void launch_up(int sg, int64_t nout, const int* owner, const int64_t* out_ptr, const int64_t* nrow, const double* A,
                const int64_t* a_off, const double* x, const int64_t* x_ptr, const int64_t* x_map, double* y,
                int64_t R, cudaStream_t s, double* recq = nullptr, int rs = 0) {
-  if (R >= 8) {  // register-blocked over 16 right-hand sides, 4 lanes per row
-    const int64_t thr = std::max<int64_t>(nout * ((R + 15) / 16), 1) * 4;
-    up_rows<4, 16><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R);
+  if (R >= 8) {  // register-blocked over H2B_UP_RB right-hand sides, H2B_UP_SG lanes per row
+    const int64_t thr = std::max<int64_t>(nout * ((R + H2B_UP_RB - 1) / H2B_UP_RB), 1) * H2B_UP_SG;
+    up_rows<H2B_UP_SG, H2B_UP_RB><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R);
     CKL();
     return;
   }
@@ -677,7 +694,7 @@ void matvec(DevH2& h, const double* w, double* u, int64_t R, cudaStream_t s) {
     const DevH2Level& HL = h.lv[l];
     const DevH2Level& HC = h.lv[l + 1];
     if (R >= 8)
-      down_rows<16><<<nblk(HC.in_total * ((R + 15) / 16), 256), 256, 0, s>>>(
+      down_rows<H2B_DN_RB><<<nblk(HC.in_total * ((R + H2B_DN_RB - 1) / H2B_DN_RB), 256), 256, 0, s>>>(
           HC.in_total, h.own_in[l + 1].get(), Lc.parent.get(), Lv.ch_ptr.get(), HC.in_ptr.get(), HL.in_ptr.get(),
           HL.kin.get(), HL.m_in.get(), HL.pmat.get(), HL.pm_off.get(), h.uin[l].get(), h.uin[l + 1].get(), R);
     else {
@@ -718,7 +735,7 @@ void matvec(DevH2& h, const double* w, double* u, int64_t R, cudaStream_t s) {
                                                far ? HL->in_ptr.get() : nullptr, far ? h.uin[L].get() : nullptr,
                                                h.near.get(), T.t_perm.get(), u, R);
     };
-    if (R >= 8) l2p(l2p_rows<16>, T.np * ((R + 15) / 16));
+    if (R >= 8) l2p(l2p_rows<H2B_L2P_RB>, T.np * ((R + H2B_L2P_RB - 1) / H2B_L2P_RB));
     else l2p(l2p_rows<1>, T.np * R);
     CKL();
   }

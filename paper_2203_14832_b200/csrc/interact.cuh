@@ -586,6 +586,21 @@ __global__ void pack_records(const PackTab* __restrict__ pt, int nlists, int64_t
   for (int q = 0; q < NR; q++) r[D + q] = T.q[i * R + r0 + q];
 }
 
+// per-matvec charge pack, one thread per (record, RHS): coalesced reads of the RHS rows and writes of the
+// record's charge slots (the thread-per-record form strides 8 * R bytes per lane on both sides)
+template <int D, int NR>
+__global__ void pack_charges(const PackTab* __restrict__ pt, int nlists, int64_t total, int64_t R, int64_t r0) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= total * NR) return;
+  const int64_t e = g / NR;
+  const int q = (int)(g - e * NR);
+  int l = 0;
+  while (l + 1 < nlists && pt[l + 1].off <= e) l++;
+  const PackTab& T = pt[l];
+  const int64_t i = e - T.off;
+  reinterpret_cast<double*>(T.rec + i * SrcRec<D, NR>::W)[D + q] = T.q[i * R + r0 + q];
+}
+
 template <int D, int KIND, int NR, int TILE, bool F32S>
 void launch_chunk(const DevH2& h, int64_t R, int64_t r0, const KParams& kp, cudaStream_t s) {
   if (!h.n_items) return;
@@ -609,8 +624,12 @@ void launch_chunk(const DevH2& h, int64_t R, int64_t r0, const KParams& kp, cuda
   // pack this chunk's charges into the records
   const auto& pk = NR == 1 ? h.pack1 : h.pack16;
   if (pk.total && !(NR == 1 && R == 1)) {  // one RHS: gather / upward pass already wrote the charges
-    pack_records<D, NR><<<nblk(pk.total, 256), 256, 0, s>>>(reinterpret_cast<const PackTab*>(pk.tabs.get()),
-                                                            pk.nlists, pk.total, R, r0, 0);
+    if (NR > 1)
+      pack_charges<D, NR><<<nblk(pk.total * NR, 256), 256, 0, s>>>(reinterpret_cast<const PackTab*>(pk.tabs.get()),
+                                                                   pk.nlists, pk.total, R, r0);
+    else
+      pack_records<D, NR><<<nblk(pk.total, 256), 256, 0, s>>>(reinterpret_cast<const PackTab*>(pk.tabs.get()),
+                                                              pk.nlists, pk.total, R, r0, 0);
     CKL();
   }
   CK(cudaMemsetAsync(h.work_counter.get(), 0, sizeof(unsigned long long), s));

@@ -65,6 +65,13 @@ CASES = [
     # name, points, sources, kernel, eps, nu, force_general, nrhs
     dict(name="u2d_reglog", P=lambda: sampling.uniform_points(4096, 2, 0), kernel="reg-log-2d", eps=1e-8, nu=64),
     dict(name="u2d_log", P=lambda: sampling.uniform_points(2048, 2, 0), kernel="log", eps=1e-8, nu=64),
+    # BASELINE.json configs[0] exactly: 2D, N=4096 uniform in [-1,1]^2 (seed 0), K = log r with K(x,x) = 0,
+    # nu = 64, NNCA tolerance 1e-8, one N(0,1) right-hand side
+    dict(name="c0_log", P=lambda: sampling.uniform_points(4096, 2, 0), kernel="log", eps=1e-8, nu=64),
+    # the headline distribution (BASELINE configs[2]: unit sphere, seed 2, eps 1e-6) at N = 32768 through the
+    # reference's compiled core (built-in 1/r)
+    dict(name="sphere32k_coulomb", P=lambda: sampling.sphere_points(32768, 3, 2), kernel="coulomb-3d", eps=1e-6,
+         nu=64),
     dict(name="u3d_coulomb", P=lambda: sampling.uniform_points(4096, 3, 1), kernel="coulomb-3d", eps=1e-8, nu=64),
     dict(name="u3d_laplace", P=lambda: sampling.uniform_points(1500, 3, 1), kernel="laplace-3d", eps=1e-8, nu=64),
     dict(name="sphere_coulomb", P=lambda: sampling.sphere_points(4096, 3, 2), kernel="coulomb-3d", eps=1e-6, nu=64),

@@ -53,7 +53,7 @@ def test_tree_matches_reference(oracle_mod, name):
         assert np.array_equal(t.get(level, "il_idx"), g[f"L{level}_interaction_list"])
 
 
-@pytest.mark.parametrize("name", [n for n in golden_names() if n not in ("dup1d", "dup2d_error")])
+@pytest.mark.parametrize("name", [n for n in golden_names() if n != "dup2d_error"])
 def test_pivots_and_matvec_match_reference(oracle_mod, name):
     g = load_golden(name)
     t = build(oracle_mod, g)
@@ -73,20 +73,19 @@ def test_pivots_and_matvec_match_reference(oracle_mod, name):
             same = all(np.array_equal(mine[a_][op[a_][c]:op[a_][c + 1]], g[f"P{level}_{a_}"][ptr[a_][c]:ptr[a_][c + 1]])
                        for a_ in op)
             mism += not same
-    if str(g["kernel"]) in BUILTIN:
-        assert mism == 0, f"{mism}/{total} cells differ"
-        st = h.stats()
-        assert st["evals_pivots"] == int(g["stat_evals_pivots"])
-        assert st["evals_couplings"] == int(g["stat_evals_couplings"])
-        assert st["evals_nearfield"] == int(g["stat_evals_nearfield"])
-        assert st["max_rank"] == int(g["stat_max_rank"])
-        assert st["cells_visited"] == int(g["stat_cells_visited"])
-        assert int(g["stat_evals_transfers"]) == 0
-    else:
-        assert mism <= max(2, total // 20), f"{mism}/{total} cells differ"
+    # every golden, built-in or custom kernel, pins every pivot set: 0 differing cells (the custom kernels
+    # ran through the reference's numpy/BLAS ACA; no near-tie resolved differently on any case)
+    assert mism == 0, f"{mism}/{total} cells differ"
+    st = h.stats()
+    assert st["evals_pivots"] == int(g["stat_evals_pivots"])
+    assert st["evals_couplings"] == int(g["stat_evals_couplings"])
+    assert st["evals_nearfield"] == int(g["stat_evals_nearfield"])
+    assert st["max_rank"] == int(g["stat_max_rank"])
+    assert st["cells_visited"] == int(g["stat_cells_visited"])
+    assert int(g["stat_evals_transfers"]) == 0
     U = h.matvec(g["W"])
     err = np.linalg.norm(U - g["U"]) / np.linalg.norm(g["U"])
-    assert err <= (1e-12 if mism == 0 else 10 * float(g["eps"])), err
+    assert err <= 1e-12, err
     # and the H2 approximation itself against the dense product
     errd = np.linalg.norm(U - g["U_dense"]) / np.linalg.norm(g["U_dense"])
     errd_ref = np.linalg.norm(g["U"] - g["U_dense"]) / np.linalg.norm(g["U_dense"])

@@ -104,6 +104,14 @@ struct DevH2 {
   std::vector<DBuf<int>> m_sb, m_end, m_cnt;       // per interaction list: member tables (interact.cuh LevelTab)
   RecSet pack1, pack16;                     // source records for RHS chunks of width 1 / 16
   DBuf<unsigned long long> work_counter;    // persistent interaction kernel: next work item
+  // symmetric one-RHS interaction kernel (interact_sym.cuh): upper member tables per list (partners Y > X),
+  // work items (list, cell) by descending pair count, descriptors and per-list tables
+  std::vector<DBuf<int>> u_sb, u_end, u_cnt;
+  DBuf<int64_t> sym_items;
+  DBuf<int> sym_desc;
+  int64_t n_sym_items = 0;
+  DBuf<unsigned char> sym_tabs;
+  bool sym_ready = false;
 };
 
 // tree.cu

@@ -1,11 +1,15 @@
 // interact_d2.cu — instantiates the interaction kernel for D = 2.
-#include "interact.cuh"
+#include "interact_sym.cuh"
 
 namespace h2b {
 template <>
 void interact_all_d<2>(int kind, const DevH2& h, int64_t R, int64_t r0, int nr, const KParams& kp,
                         cudaStream_t s) {
   interact_all_d_impl<2>(kind, h, R, r0, nr, kp, s);
+}
+template <>
+void interact_sym_d<2>(int kind, const DevH2& h, int64_t R, int64_t r0, const KParams& kp, cudaStream_t s) {
+  interact_sym_d_impl<2>(kind, h, R, r0, kp, s);
 }
 template <>
 void pack_coords_dim<2>(const DevH2& h, int nr, cudaStream_t s) {

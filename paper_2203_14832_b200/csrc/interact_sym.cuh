@@ -1,0 +1,364 @@
+// interact_sym.cuh — symmetric interaction kernel (one right-hand side).
+//
+// On the symmetric path (symmetric kernel on shared points, compress.py:229)
+// the outgoing pivots of a cell are its incoming ones (s_out = t_in,
+// compress.py:254-260), so the coupling blocks satisfy S_{Y,X} = S_{X,Y}^T
+// and the near-field blocks K(Y, X) = K(X, Y)^T.  The reference evaluates
+// and applies both ordered blocks (compress.py:307-328, matvec.py:161); here
+// each unordered cell pair {X, Y} is evaluated once, by the work item of the
+// lower cell (Y > X in the engine's Morton order), and applied in both
+// directions:
+//     u_in^X += S_{X,Y} w_out^Y      (row sums: X's targets)
+//     u_in^Y += S_{X,Y}^T w_out^X    (column sums: Y's targets)
+// which halves the kernel evaluations (r^2 + rsqrt + Newton) per product.
+//
+// Work item = (list, cell X): list l in [2, L] is level l's interaction list,
+// L + 1 the leaf near field (neighbour leaves Y > X, difference-form r^2),
+// L + 2 the leaf self block K(X, X) (row sums only, r2 == 0 -> 0, the
+// punctured diagonal).  One warp per item.  X's targets are staged TB at a
+// time in the warp's shared memory and broadcast; the "upper" partners'
+// source records (contiguous Morton ranges, adjacent ones merged) are spread
+// over the lanes, RS records per lane held in registers with their column
+// accumulators.  Per (target, lane) the lane evaluates RS pairs:
+//     r2  = |x'|^2 + |y'|^2 - 2 x'.y'            (M2L; DADD + 3 DFMA)
+//     K   = K(r2)                                 (1/r: FP32 seed, DMUL, DFMA, DMUL)
+//     col_s += K q_t ;  p_t += K q_s              (2 DFMA)
+// 9 FP64 instructions per unordered pair = 4.5 per applied entry (the
+// one-directional kernel, interact.cuh, needs 8).  The TB row partials p_t
+// live in registers for the whole chunk and are reduced across the warp once
+// per chunk (butterfly reduce-scatter); column sums are flushed after every
+// pass.  Both go to the level's u_in (and the near-field buffer) with FP64
+// reductions (RED.ADD.F64), so those buffers are zeroed first.
+#pragma once
+#include "interact.cuh"
+
+namespace h2b {
+namespace {
+
+#ifndef H2B_SYM_RS
+#define H2B_SYM_RS 3
+#endif
+#ifndef H2B_SYM_TB
+#define H2B_SYM_TB 16
+#endif
+#ifndef H2B_SYM_MINB
+#define H2B_SYM_MINB 4
+#endif
+constexpr int SYM_THREADS = 128;
+constexpr int SYM_MAXMEM = 256;  // members staged per chunk of a cell's upper list
+
+// Per-list tables of the symmetric kernel (device copy, one per list id).
+struct SymTab {
+  const double2* rec;  // source records [y_0..y_{D-1}, q] (SrcRec<D, 1>) of this list's points
+  const int64_t* ptr;  // record range per cell (targets == sources on the symmetric path)
+  const int* m_sb;     // upper member tables: first record of each (merged) member
+  const int* m_end;    //   inclusive prefix of member lengths within the cell's segment
+  double* out;         // result rows (record index) * R + r0
+};
+
+enum SymMode { SYM_M2L = 0, SYM_NEAR = 1, SYM_SELF = 2 };
+
+template <int D>
+struct alignas(16) SymTgt {  // one staged target: M2L a = (-2 x', |x'|^2), near a = x'
+  static constexpr int A = D + 1;
+  static constexpr int N2 = 2 * ((A + 1 + 1) / 2);  // doubles incl. q, padded to 16 bytes
+  double v[N2];
+};
+
+template <int D>
+struct alignas(16) SymWarp {
+  SymTgt<D> tgt[H2B_SYM_TB];
+  int pref[SYM_MAXMEM + 1];
+  int sbeg[SYM_MAXMEM];
+};
+
+template <int D>
+__device__ __forceinline__ void load_rec(const double2* rec, int64_t i, double (&y)[D], double& q) {
+  constexpr int W = SrcRec<D, 1>::W;
+  double v[2 * W];
+#pragma unroll
+  for (int w = 0; w < W; w++) {
+    const double2 u = __ldg(rec + i * W + w);
+    v[2 * w] = u.x;
+    v[2 * w + 1] = u.y;
+  }
+#pragma unroll
+  for (int k = 0; k < D; k++) y[k] = v[k];
+  q = v[D];
+}
+
+// K(r2) in the kernel's accumulation units (1/r: "2/r", scaled at the flush)
+template <int KIND, int MODE, bool F32S>
+__device__ __forceinline__ double sym_kval(double r2, const KParams& kp) {
+  if constexpr (is_inv_r<KIND>()) {
+    if constexpr (MODE == SYM_SELF) {
+      const bool zero = __double2hiint(r2) == 0;  // r2 == 0 (or subnormal): the punctured diagonal
+      const double r2s = zero ? 1.0 : r2;
+      const double y = rsq_approx(r2s);
+      const double kv = y * fma(-r2s, y * y, 3.0);
+      return zero ? 0.0 : kv;
+    } else if constexpr (MODE == SYM_M2L && F32S) {
+      const double y = rsq_seed_f32(r2);  // FP32 seed + quadratic step (interact.cuh rsq_seed_f32)
+      return y * fma(-r2, y * y, 3.0);
+    } else if constexpr (MODE == SYM_M2L) {
+      const double y = rsq_approx(r2);  // FP64 seed + cubic step (multipole charges amplify a bias)
+      const double e = fma(-r2, y * y, 1.0);
+      return y * fma(e, fma(0.75, e, 1.0), 2.0);
+    } else {  // near field between distinct leaves: r2 > 0, plain input charges
+      const double y = rsq_approx(r2);
+      return y * fma(-r2, y * y, 3.0);
+    }
+  } else {
+    return kfast<KIND>(r2, kp);
+  }
+}
+
+// One work item on one warp.
+template <int D, int KIND, int RS, int TB, bool F32S, int MODE>
+__device__ __forceinline__ void sym_item(const SymTab& T, int4 dsc, int64_t R, int64_t r0, const KParams& kp,
+                                         SymWarp<D>& S) {
+  constexpr double SCALE = kscale<KIND>() * (is_inv_r<KIND>() ? 0.5 : 1.0);
+  constexpr int NV = SymTgt<D>::N2;
+  const int lane = threadIdx.x & 31;
+  const int tb = dsc.x, m = dsc.y, lb = dsc.z, cnt = dsc.w;
+  double o[D];  // frame origin: the item's first target
+  {
+    double q;
+    load_rec<D>(T.rec, tb, o, q);
+  }
+  const int nchunk_m = MODE == SYM_SELF ? 1 : (cnt + SYM_MAXMEM - 1) / SYM_MAXMEM;
+  for (int tc0 = 0; tc0 < m; tc0 += TB) {
+    const int tcnt = m - tc0 < TB ? m - tc0 : TB;
+    __syncwarp();
+    if (lane < tcnt) {  // stage this chunk's targets
+      double x[D], q;
+      load_rec<D>(T.rec, tb + tc0 + lane, x, q);
+      double* v = S.tgt[lane].v;
+      double n2 = 0.0;
+#pragma unroll
+      for (int k = 0; k < D; k++) {
+        const double dk = x[k] - o[k];
+        n2 = fma(dk, dk, n2);
+        v[k] = MODE == SYM_M2L ? -2.0 * dk : dk;
+      }
+      v[D] = n2;
+      v[D + 1] = q;
+    }
+    double p[TB];
+#pragma unroll
+    for (int t = 0; t < TB; t++) p[t] = 0.0;
+    for (int mc = 0; mc < nchunk_m; mc++) {
+      int nmem;
+      __syncwarp();
+      if constexpr (MODE == SYM_SELF) {  // the cell itself
+        nmem = 1;
+        if (lane == 0) {
+          S.sbeg[0] = tb;
+          S.pref[0] = 0;
+          S.pref[1] = m;
+        }
+      } else {
+        const int q0 = mc * SYM_MAXMEM;
+        nmem = cnt - q0 < SYM_MAXMEM ? cnt - q0 : SYM_MAXMEM;
+        const int base = q0 == 0 ? 0 : T.m_end[lb + q0 - 1];
+        for (int i = lane; i < nmem; i += 32) {
+          S.sbeg[i] = T.m_sb[lb + q0 + i];
+          S.pref[i + 1] = T.m_end[lb + q0 + i] - base;
+        }
+        if (lane == 0) S.pref[0] = 0;
+      }
+      __syncwarp();
+      const int total = S.pref[nmem];
+      int cur = 0;  // member cursor (slots visited in increasing order)
+      for (int pb = 0; pb < total; pb += 32 * RS) {
+        double y[RS][D], yy[RS], qs[RS], col[RS];
+        int64_t gidx[RS];
+        bool ok[RS];
+#pragma unroll
+        for (int s = 0; s < RS; s++) {
+          int j = pb + lane + 32 * s;
+          ok[s] = j < total;
+          if (!ok[s]) j = pb;  // dummy slot: a copy of the pass's first source with zero charge
+          int c = ok[s] ? cur : 0;
+          while (S.pref[c + 1] <= j) c++;
+          if (ok[s]) cur = c;
+          gidx[s] = (int64_t)S.sbeg[c] + (j - S.pref[c]);
+          double yv[D], q;
+          load_rec<D>(T.rec, gidx[s], yv, q);
+          double n2 = 0.0;
+#pragma unroll
+          for (int k = 0; k < D; k++) {
+            y[s][k] = yv[k] - o[k];
+            n2 = fma(y[s][k], y[s][k], n2);
+          }
+          yy[s] = n2;
+          qs[s] = ok[s] ? q : 0.0;
+          col[s] = 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < TB; t++) {
+          if (t >= tcnt) break;
+          double a[NV];
+#pragma unroll
+          for (int i = 0; i < NV; i += 2) {
+            const double2 u = *reinterpret_cast<const double2*>(&S.tgt[t].v[i]);
+            a[i] = u.x;
+            a[i + 1] = u.y;
+          }
+#pragma unroll
+          for (int s = 0; s < RS; s++) {
+            double r2;
+            if constexpr (MODE == SYM_M2L) {
+              r2 = a[D] + yy[s];
+#pragma unroll
+              for (int k = 0; k < D; k++) r2 = fma(a[k], y[s][k], r2);
+            } else {
+              r2 = 0.0;
+#pragma unroll
+              for (int k = 0; k < D; k++) {
+                const double dk = a[k] - y[s][k];
+                r2 = fma(dk, dk, r2);
+              }
+            }
+            const double kv = sym_kval<KIND, MODE, F32S>(r2, kp);
+            if constexpr (MODE != SYM_SELF) col[s] = fma(kv, a[D + 1], col[s]);
+            p[t] = fma(kv, qs[s], p[t]);
+          }
+        }
+        if constexpr (MODE != SYM_SELF) {
+#pragma unroll
+          for (int s = 0; s < RS; s++)
+            if (ok[s]) atomicAdd(T.out + gidx[s] * R + r0, col[s] * SCALE);
+        }
+      }
+    }
+    // reduce the TB row partials over the warp: reduce-scatter (lane >> 1 ends up holding target lane >> 1 for
+    // TB = 16), then add into the targets' rows
+    static_assert(TB == 16, "reduce-scatter written for TB = 16");
+    double v8[8], v4[4], v2[2], v1;
+    {
+      const bool hi = lane & 16;
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        const double send = hi ? p[i] : p[i + 8];
+        const double keep = hi ? p[i + 8] : p[i];
+        v8[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+      }
+    }
+    {
+      const bool hi = lane & 8;
+#pragma unroll
+      for (int i = 0; i < 4; i++) {
+        const double send = hi ? v8[i] : v8[i + 4];
+        const double keep = hi ? v8[i + 4] : v8[i];
+        v4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+      }
+    }
+    {
+      const bool hi = lane & 4;
+#pragma unroll
+      for (int i = 0; i < 2; i++) {
+        const double send = hi ? v4[i] : v4[i + 2];
+        const double keep = hi ? v4[i + 2] : v4[i];
+        v2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+      }
+    }
+    {
+      const bool hi = lane & 2;
+      const double send = hi ? v2[0] : v2[1];
+      const double keep = hi ? v2[1] : v2[0];
+      v1 = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    }
+    v1 += __shfl_xor_sync(0xffffffffu, v1, 1);
+    const int t = lane >> 1;
+    if ((lane & 1) == 0 && t < tcnt) atomicAdd(T.out + (int64_t)(tb + tc0 + t) * R + r0, v1 * SCALE);
+  }
+}
+
+// Persistent kernel: warps pull (list, cell) items by descending pair count.
+template <int D, int KIND, int RS, int TB, bool F32S>
+__global__ void __launch_bounds__(SYM_THREADS, H2B_SYM_MINB)
+    interact_sym(const int64_t* __restrict__ items, const int4* __restrict__ descs, int64_t n_items,
+                 unsigned long long* __restrict__ counter, const SymTab* __restrict__ tabs, int ntabs, int near_list,
+                 int self_list, int64_t R, int64_t r0, KParams kp) {
+  __shared__ SymTab tab_s[32];
+  __shared__ SymWarp<D> ws[SYM_THREADS / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < ntabs; i += blockDim.x) tab_s[i] = tabs[i];
+  __syncthreads();
+  SymWarp<D>& S = ws[warp];
+  for (;;) {
+    unsigned long long idx = 0;
+    if (lane == 0) idx = atomicAdd(counter, 1ull);
+    idx = __shfl_sync(0xffffffffu, idx, 0);
+    if (idx >= (unsigned long long)n_items) break;
+    const int lst = (int)(items[idx] >> 40);
+    const int4 dsc = descs[idx];
+    const SymTab& T = tab_s[lst];
+    if (lst == self_list)
+      sym_item<D, KIND, RS, TB, F32S, SYM_SELF>(T, dsc, R, r0, kp, S);
+    else if (lst == near_list)
+      sym_item<D, KIND, RS, TB, F32S, SYM_NEAR>(T, dsc, R, r0, kp, S);
+    else
+      sym_item<D, KIND, RS, TB, F32S, SYM_M2L>(T, dsc, R, r0, kp, S);
+  }
+}
+
+template <int D, int KIND, bool F32S>
+void launch_sym(const DevH2& h, int64_t R, int64_t r0, const KParams& kp, cudaStream_t s) {
+  if (!h.n_sym_items) return;
+  const int L = h.t->depth;
+  auto kern = interact_sym<D, KIND, H2B_SYM_RS, H2B_SYM_TB, F32S>;
+  int dev = 0, nsm = 0, per = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, SYM_THREADS, 0));
+  const int64_t grid = std::min<int64_t>((int64_t)nsm * std::max(per, 1),
+                                         (h.n_sym_items + SYM_THREADS / 32 - 1) / (SYM_THREADS / 32));
+  // one RHS of a wider product: pack this column's charges into the records (the gather / upward pass wrote
+  // them already when R == 1)
+  const auto& pk = h.pack1;
+  if (pk.total && R != 1) {
+    pack_records<D, 1><<<nblk(pk.total, 256), 256, 0, s>>>(reinterpret_cast<const PackTab*>(pk.tabs.get()),
+                                                           pk.nlists, pk.total, R, r0, 0);
+    CKL();
+  }
+  CK(cudaMemsetAsync(h.work_counter.get(), 0, sizeof(unsigned long long), s));
+  kern<<<(unsigned)grid, SYM_THREADS, 0, s>>>(h.sym_items.get(), reinterpret_cast<const int4*>(h.sym_desc.get()),
+                                              h.n_sym_items, h.work_counter.get(),
+                                              reinterpret_cast<const SymTab*>(h.sym_tabs.get()), L + 3, L + 1, L + 2,
+                                              R, r0, kp);
+  CKL();
+}
+
+template <int D, int KIND>
+void launch_sym_kind(const DevH2& h, int64_t R, int64_t r0, const KParams& kp, cudaStream_t s) {
+  if constexpr (is_inv_r<KIND>()) {
+    if (f32seed_ok(h)) {
+      launch_sym<D, KIND, true>(h, R, r0, kp, s);
+      return;
+    }
+  }
+  launch_sym<D, KIND, false>(h, R, r0, kp, s);
+}
+
+template <int D>
+void interact_sym_d_impl(int kind, const DevH2& h, int64_t R, int64_t r0, const KParams& kp, cudaStream_t s) {
+  switch (kind) {
+    case COULOMB: launch_sym_kind<D, COULOMB>(h, R, r0, kp, s); break;
+    case LAPLACE: launch_sym_kind<D, LAPLACE>(h, R, r0, kp, s); break;
+    case GAUSSIAN: launch_sym_kind<D, GAUSSIAN>(h, R, r0, kp, s); break;
+    case GAUSSIAN_SCALED: launch_sym_kind<D, GAUSSIAN_SCALED>(h, R, r0, kp, s); break;
+    case MATERN: launch_sym_kind<D, MATERN>(h, R, r0, kp, s); break;
+    case LOG: launch_sym_kind<D, LOG>(h, R, r0, kp, s); break;
+    case REG_INVERSE: launch_sym_kind<D, REG_INVERSE>(h, R, r0, kp, s); break;
+    default: launch_sym_kind<D, REG_LOG>(h, R, r0, kp, s); break;
+  }
+}
+
+}  // namespace
+
+template <int D>
+void interact_sym_d(int kind, const DevH2& h, int64_t R, int64_t r0, const KParams& kp, cudaStream_t s);
+
+}  // namespace h2b

@@ -14,7 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 
-#include "interact.cuh"
+#include "interact_sym.cuh"
 
 namespace h2b {
 
@@ -316,6 +316,15 @@ void interact_all(int d, int kind, const DevH2& h, int64_t R, int64_t r0, int nr
   }
 }
 
+void interact_sym_all(int d, int kind, const DevH2& h, int64_t R, int64_t r0, const KParams& kp, cudaStream_t s) {
+  switch (d) {
+    case 1: interact_sym_d<1>(kind, h, R, r0, kp, s); break;
+    case 2: interact_sym_d<2>(kind, h, R, r0, kp, s); break;
+    case 3: interact_sym_d<3>(kind, h, R, r0, kp, s); break;
+    default: interact_sym_d<4>(kind, h, R, r0, kp, s); break;
+  }
+}
+
 void pack_coords(int d, const DevH2& h, int nr, cudaStream_t s) {
   switch (d) {
     case 1: pack_coords_dim<1>(h, nr, s); break;
@@ -331,8 +340,8 @@ void pack_coords(int d, const DevH2& h, int nr, cudaStream_t s) {
 // interaction kernel issues one TMA bulk copy for the run (merge = 0 keeps one entry per list member).  The
 // near field's own leaf is dropped (it is handled by the r2 == 0 pass).
 __global__ void member_tables(int64_t n, const int64_t* __restrict__ l_ptr, const int64_t* __restrict__ l_idx,
-                              const int64_t* __restrict__ s_ptr, int self_zero, int merge, int* __restrict__ m_sb,
-                              int* __restrict__ m_end, int* __restrict__ m_cnt) {
+                              const int64_t* __restrict__ s_ptr, int self_zero, int merge, int upper,
+                              int* __restrict__ m_sb, int* __restrict__ m_end, int* __restrict__ m_cnt) {
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= n) return;
   const int64_t q0 = l_ptr[c];
@@ -341,6 +350,7 @@ __global__ void member_tables(int64_t n, const int64_t* __restrict__ l_ptr, cons
   for (int64_t q = q0; q < l_ptr[c + 1]; q++) {
     const int64_t y = l_idx[q];
     if (self_zero && y == c) continue;
+    if (upper && y <= c) continue;  // symmetric kernel: the pair {c, y} belongs to the lower cell
     const int64_t b = s_ptr[y], e = s_ptr[y + 1];
     if (e == b) continue;
     run += (int)(e - b);
@@ -371,6 +381,45 @@ __global__ void item_costs(int64_t n, int lev, const int64_t* __restrict__ t_ptr
   const int64_t m = t_ptr[c + 1] - t_ptr[c];
   cost[c] = m > 0 ? (unsigned long long)(m * src) + 1ull : 0ull;
   item[c] = ((int64_t)lev << 40) | c;
+}
+
+// symmetric kernel work items: (list, cell) with cost = targets x upper-partner sources (self block: m^2)
+__global__ void sym_costs(int64_t n, int lst, int self, const int64_t* __restrict__ ptr,
+                          const int64_t* __restrict__ l_ptr, const int64_t* __restrict__ l_idx,
+                          unsigned long long* __restrict__ cost, int64_t* __restrict__ item) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const int64_t m = ptr[c + 1] - ptr[c];
+  int64_t src = 0;
+  if (self) {
+    src = m;
+  } else {
+    for (int64_t q = l_ptr[c]; q < l_ptr[c + 1]; q++) {
+      const int64_t y = l_idx[q];
+      if (y > c) src += ptr[y + 1] - ptr[y];
+    }
+  }
+  cost[c] = (m > 0 && src > 0) ? (unsigned long long)(m * src) + 1ull : 0ull;
+  item[c] = ((int64_t)lst << 40) | c;
+}
+
+struct SymBuild {
+  const int64_t* ptr;
+  const int64_t* l_ptr;
+  const int* u_cnt;
+};
+
+__global__ void make_sym_desc(const int64_t* __restrict__ items, int64_t n, const SymBuild* __restrict__ sb,
+                              int self_list, int4* __restrict__ desc) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t it = items[i];
+  const int lst = (int)(it >> 40);
+  const int64_t c = it & ((1ll << 40) - 1);
+  const SymBuild& B = sb[lst];
+  const int64_t tb = B.ptr[c];
+  const bool self = lst == self_list;
+  desc[i] = make_int4((int)tb, (int)(B.ptr[c + 1] - tb), self ? 0 : (int)B.l_ptr[c], self ? 0 : B.u_cnt[c]);
 }
 
 KParams make_kp(int kind, double a) {
@@ -426,6 +475,108 @@ void build_items(DevH2& h, cudaStream_t s) {
   int64_t nz = 0;
   while (nz < total && hc[nz] > 0) nz++;
   h.n_items = nz;
+}
+
+// Symmetric kernel (interact_sym.cuh): upper member tables, work items by descending pair count and their
+// descriptors.  Static per H2 matrix.  List ids: 2..L = M2L levels, L + 1 = near field, L + 2 = self blocks.
+void build_sym(DevH2& h, cudaStream_t s) {
+  const DevTree& T = *h.t;
+  const int L = T.depth;
+  h.u_sb.clear();
+  h.u_end.clear();
+  h.u_cnt.clear();
+  h.u_sb.resize(L + 3);
+  h.u_end.resize(L + 3);
+  h.u_cnt.resize(L + 3);
+  std::vector<SymBuild> sb(L + 3);
+  std::memset(sb.data(), 0, sizeof(SymBuild) * sb.size());
+  std::vector<int> ids;
+  for (int l = 2; l <= L; l++) ids.push_back(l);
+  ids.push_back(L + 1);
+  for (int l : ids) {
+    const bool nf = l == L + 1;
+    const DevLevel& Lv = T.lv[nf ? L : l];
+    const int64_t tot = nf ? Lv.nb_total : Lv.il_total;
+    const int64_t* ptr = nf ? Lv.t_ptr.get() : h.lv[l].in_ptr.get();
+    h.u_sb[l].alloc(std::max<int64_t>(tot, 1), &h.mem);
+    h.u_end[l].alloc(std::max<int64_t>(tot, 1), &h.mem);
+    h.u_cnt[l].alloc(std::max<int64_t>(Lv.n, 1), &h.mem);
+    if (Lv.n)
+      member_tables<<<nblk(Lv.n, 256), 256, 0, s>>>(Lv.n, nf ? Lv.nb_ptr.get() : Lv.il_ptr.get(),
+                                                     nf ? Lv.nb_idx.get() : Lv.il_idx.get(), ptr, 0, 1, 1,
+                                                     h.u_sb[l].get(), h.u_end[l].get(), h.u_cnt[l].get());
+    CKL();
+    sb[l].ptr = ptr;
+    sb[l].l_ptr = nf ? Lv.nb_ptr.get() : Lv.il_ptr.get();
+    sb[l].u_cnt = h.u_cnt[l].get();
+  }
+  sb[L + 2].ptr = T.lv[L].t_ptr.get();
+  // items
+  int64_t total = 2 * T.lv[L].n;
+  for (int l = 2; l <= L; l++) total += T.lv[l].n;
+  DBuf<unsigned long long> cost, cost_sorted;
+  DBuf<int64_t> item;
+  cost.alloc(std::max<int64_t>(total, 1));
+  cost_sorted.alloc(std::max<int64_t>(total, 1));
+  item.alloc(std::max<int64_t>(total, 1));
+  h.sym_items.alloc(std::max<int64_t>(total, 1), &h.mem);
+  int64_t off = 0;
+  for (int l : ids) {
+    const bool nf = l == L + 1;
+    const DevLevel& Lv = T.lv[nf ? L : l];
+    if (Lv.n)
+      sym_costs<<<nblk(Lv.n, 256), 256, 0, s>>>(Lv.n, l, 0, sb[l].ptr, sb[l].l_ptr,
+                                                nf ? Lv.nb_idx.get() : Lv.il_idx.get(), cost.get() + off,
+                                                item.get() + off);
+    CKL();
+    off += Lv.n;
+  }
+  if (T.lv[L].n)
+    sym_costs<<<nblk(T.lv[L].n, 256), 256, 0, s>>>(T.lv[L].n, L + 2, 1, sb[L + 2].ptr, nullptr, nullptr,
+                                                   cost.get() + off, item.get() + off);
+  CKL();
+  size_t bytes = 0;
+  CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, cost.get(), cost_sorted.get(), item.get(),
+                                               h.sym_items.get(), total, 0, 64, s));
+  DBuf<unsigned char> tmp;
+  tmp.alloc(std::max<size_t>(bytes, 1));
+  CK(cub::DeviceRadixSort::SortPairsDescending(tmp.get(), bytes, cost.get(), cost_sorted.get(), item.get(),
+                                               h.sym_items.get(), total, 0, 64, s));
+  auto hc = to_host(cost_sorted.get(), total, s);
+  int64_t nz = 0;
+  while (nz < total && hc[nz] > 0) nz++;
+  h.n_sym_items = nz;
+  DBuf<SymBuild> dsb;
+  dsb.alloc(sb.size());
+  CK(cudaMemcpyAsync(dsb.get(), sb.data(), sizeof(SymBuild) * sb.size(), cudaMemcpyHostToDevice, s));
+  h.sym_desc.alloc(4 * std::max<int64_t>(nz, 1), &h.mem);
+  if (nz)
+    make_sym_desc<<<nblk(nz, 256), 256, 0, s>>>(h.sym_items.get(), nz, dsb.get(), L + 2,
+                                                reinterpret_cast<int4*>(h.sym_desc.get()));
+  CKL();
+  CK(cudaStreamSynchronize(s));
+  h.sym_ready = true;
+}
+
+// per-list tables of the symmetric kernel (records and outputs change when the scratch is rebuilt)
+void build_sym_tabs(DevH2& h, cudaStream_t s) {
+  const DevTree& T = *h.t;
+  const int L = T.depth;
+  std::vector<SymTab> tabs(L + 3);
+  std::memset(tabs.data(), 0, sizeof(SymTab) * tabs.size());
+  for (int l = 2; l <= L + 2; l++) {
+    SymTab& t = tabs[l];
+    const bool leaf = l > L;
+    t.rec = h.pack1.lists[leaf ? std::max(L - 1, 0) : l - 2].get();
+    t.ptr = leaf ? T.lv[L].t_ptr.get() : h.lv[l].in_ptr.get();
+    if (l <= L + 1) {
+      t.m_sb = h.u_sb[l].get();
+      t.m_end = h.u_end[l].get();
+    }
+    t.out = leaf ? h.near.get() : h.uin[l].get();
+  }
+  h.sym_tabs.alloc(sizeof(SymTab) * tabs.size(), &h.mem);
+  CK(cudaMemcpyAsync(h.sym_tabs.get(), tabs.data(), sizeof(SymTab) * tabs.size(), cudaMemcpyHostToDevice, s));
 }
 
 // Source records (interact.cuh SrcRec) for RHS width nr: allocation, pack
@@ -492,7 +643,7 @@ void build_tabs(DevH2& h, int64_t R, cudaStream_t s) {
       if (Lv.n)
         member_tables<<<nblk(Lv.n, 256), 256, 0, s>>>(Lv.n, nf ? Lv.nb_ptr.get() : Lv.il_ptr.get(),
                                                          nf ? Lv.nb_idx.get() : Lv.il_idx.get(), sp, nf ? 1 : 0,
-                                                         merge, h.m_sb[l].get(), h.m_end[l].get(),
+                                                         merge, 0, h.m_sb[l].get(), h.m_end[l].get(),
                                                          h.m_cnt[l].get());
       CKL();
     }
@@ -608,6 +759,10 @@ void ensure_scratch(DevH2& h, int64_t R, cudaStream_t s) {
   if (R >= 16) build_records(h, 16, s);
   if (R % 16) build_records(h, 1, s);
   build_tabs(h, R, s);
+  if (h.symmetric && R % 16) {
+    if (!h.sym_ready) build_sym(h, s);
+    build_sym_tabs(h, s);
+  }
   h.scratch_nrhs = R;
 }
 
@@ -684,8 +839,19 @@ void matvec(DevH2& h, const double* w, double* u, int64_t R, cudaStream_t s) {
     }
   }
   if (g_profile) CK(cudaEventRecord(ev[1], s));
-  // ---- every M2L level + the near field in one launch ----
-  for (auto& ch : chunks) interact_all(d, h.kind, h, R, ch.first, ch.second, kp, s);
+  // ---- every M2L level + the near field in one launch per RHS chunk ----
+  // one-RHS chunks on the symmetric path: each unordered cell pair evaluated once (interact_sym.cuh), results
+  // accumulated with FP64 reductions into zeroed u_in / near buffers
+  const bool sym = h.symmetric && h.sym_ready && (R % 16) != 0;
+  if (sym) {
+    for (int l = 2; l <= L; l++)
+      CK(cudaMemsetAsync(h.uin[l].get(), 0, sizeof(double) * h.lv[l].in_total * R, s));
+    CK(cudaMemsetAsync(h.near.get(), 0, sizeof(double) * T.np * R, s));
+  }
+  for (auto& ch : chunks) {
+    if (sym && ch.second == 1) interact_sym_all(d, h.kind, h, R, ch.first, kp, s);
+    else interact_all(d, h.kind, h, R, ch.first, ch.second, kp, s);
+  }
   if (g_profile) CK(cudaEventRecord(ev[2], s));
   // ---- downward pass (L2L), one thread per child row ----
   for (int l = 2; l < L; l++) {

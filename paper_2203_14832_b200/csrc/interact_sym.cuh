@@ -65,11 +65,17 @@ struct alignas(16) SymTgt {  // one staged target: M2L a = (-2 x', |x'|^2), near
   double v[N2];
 };
 
+#ifndef H2B_SYM_MAP
+#define H2B_SYM_MAP 1024
+#endif
+constexpr int SYM_MAP = H2B_SYM_MAP;  // slots of a source window (record indices staged in shared memory)
+
 template <int D>
 struct alignas(16) SymWarp {
   SymTgt<D> tgt[H2B_SYM_TB];
   int pref[SYM_MAXMEM + 1];
   int sbeg[SYM_MAXMEM];
+  int map[SYM_MAP];  // window slot -> record index
 };
 
 template <int D>
@@ -113,10 +119,81 @@ __device__ __forceinline__ double sym_kval(double r2, const KParams& kp) {
   }
 }
 
-// One work item on one warp.
+// Sum of the TB = 16 row partials over the warp by a butterfly reduce-scatter: afterwards lanes 2t and
+// 2t + 1 hold the total of target t.
+__device__ __forceinline__ double warp_reduce_scatter16(const double (&p)[16], int lane) {
+  double v8[8], v4[4], v2[2];
+  {
+    const bool hi = lane & 16;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      const double send = hi ? p[i] : p[i + 8];
+      const double keep = hi ? p[i + 8] : p[i];
+      v8[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+  }
+  {
+    const bool hi = lane & 8;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      const double send = hi ? v8[i] : v8[i + 4];
+      const double keep = hi ? v8[i + 4] : v8[i];
+      v4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+  }
+  {
+    const bool hi = lane & 4;
+#pragma unroll
+    for (int i = 0; i < 2; i++) {
+      const double send = hi ? v4[i] : v4[i + 2];
+      const double keep = hi ? v4[i + 2] : v4[i];
+      v2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+  }
+  const bool hi = lane & 2;
+  double v1 = (hi ? v2[1] : v2[0]) + __shfl_xor_sync(0xffffffffu, hi ? v2[0] : v2[1], 2);
+  return v1 + __shfl_xor_sync(0xffffffffu, v1, 1);
+}
+
+// One pair: r^2, K, and both accumulations.
+template <int D, int KIND, int MODE, bool F32S, int NV>
+__device__ __forceinline__ void sym_pair(const double (&a)[NV], const double (&y)[D], double yy, double qs,
+                                         double& col, double& p, const KParams& kp) {
+  double r2;
+  if constexpr (MODE == SYM_M2L) {
+    r2 = a[D] + yy;
+#pragma unroll
+    for (int k = 0; k < D; k++) r2 = fma(a[k], y[k], r2);
+  } else {
+    r2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; k++) {
+      const double dk = a[k] - y[k];
+      r2 = fma(dk, dk, r2);
+    }
+  }
+  const double kv = sym_kval<KIND, MODE, F32S>(r2, kp);
+  if constexpr (MODE != SYM_SELF) col = fma(kv, a[D + 1], col);
+  p = fma(kv, qs, p);
+}
+
+template <int D>
+__device__ __forceinline__ void load_tgt(const SymWarp<D>& S, int t, double (&a)[SymTgt<D>::N2]) {
+#pragma unroll
+  for (int i = 0; i < SymTgt<D>::N2; i += 2) {
+    const double2 u = *reinterpret_cast<const double2*>(&S.tgt[t].v[i]);
+    a[i] = u.x;
+    a[i + 1] = u.y;
+  }
+}
+
+// One work item on one warp.  Loop nest: member chunks (<= SYM_MAXMEM members, table in shared memory) >
+// source windows (<= SYM_MAP records; slot -> record index map expanded in shared memory) > target chunks
+// (TB targets staged, padded to an even count with a zero-charge copy) > passes (RS records per lane).
 template <int D, int KIND, int RS, int TB, bool F32S, int MODE>
 __device__ __forceinline__ void sym_item(const SymTab& T, int4 dsc, int64_t R, int64_t r0, const KParams& kp,
                                          SymWarp<D>& S) {
+  static_assert(TB == 16, "reduce-scatter written for TB = 16");
   constexpr double SCALE = kscale<KIND>() * (is_inv_r<KIND>() ? 0.5 : 1.0);
   constexpr int NV = SymTgt<D>::N2;
   const int lane = threadIdx.x & 31;
@@ -127,151 +204,103 @@ __device__ __forceinline__ void sym_item(const SymTab& T, int4 dsc, int64_t R, i
     load_rec<D>(T.rec, tb, o, q);
   }
   const int nchunk_m = MODE == SYM_SELF ? 1 : (cnt + SYM_MAXMEM - 1) / SYM_MAXMEM;
-  for (int tc0 = 0; tc0 < m; tc0 += TB) {
-    const int tcnt = m - tc0 < TB ? m - tc0 : TB;
+  for (int mc = 0; mc < nchunk_m; mc++) {
+    int nmem;
     __syncwarp();
-    if (lane < tcnt) {  // stage this chunk's targets
-      double x[D], q;
-      load_rec<D>(T.rec, tb + tc0 + lane, x, q);
-      double* v = S.tgt[lane].v;
-      double n2 = 0.0;
-#pragma unroll
-      for (int k = 0; k < D; k++) {
-        const double dk = x[k] - o[k];
-        n2 = fma(dk, dk, n2);
-        v[k] = MODE == SYM_M2L ? -2.0 * dk : dk;
+    if constexpr (MODE == SYM_SELF) {  // the cell itself
+      nmem = 1;
+      if (lane == 0) {
+        S.sbeg[0] = tb;
+        S.pref[0] = 0;
+        S.pref[1] = m;
       }
-      v[D] = n2;
-      v[D + 1] = q;
+    } else {
+      const int q0 = mc * SYM_MAXMEM;
+      nmem = cnt - q0 < SYM_MAXMEM ? cnt - q0 : SYM_MAXMEM;
+      const int base = q0 == 0 ? 0 : T.m_end[lb + q0 - 1];
+      for (int i = lane; i < nmem; i += 32) {
+        S.sbeg[i] = T.m_sb[lb + q0 + i];
+        S.pref[i + 1] = T.m_end[lb + q0 + i] - base;
+      }
+      if (lane == 0) S.pref[0] = 0;
     }
-    double p[TB];
-#pragma unroll
-    for (int t = 0; t < TB; t++) p[t] = 0.0;
-    for (int mc = 0; mc < nchunk_m; mc++) {
-      int nmem;
+    __syncwarp();
+    const int total = S.pref[nmem];
+    for (int w0 = 0; w0 < total; w0 += SYM_MAP) {
+      const int wn = total - w0 < SYM_MAP ? total - w0 : SYM_MAP;
       __syncwarp();
-      if constexpr (MODE == SYM_SELF) {  // the cell itself
-        nmem = 1;
-        if (lane == 0) {
-          S.sbeg[0] = tb;
-          S.pref[0] = 0;
-          S.pref[1] = m;
-        }
-      } else {
-        const int q0 = mc * SYM_MAXMEM;
-        nmem = cnt - q0 < SYM_MAXMEM ? cnt - q0 : SYM_MAXMEM;
-        const int base = q0 == 0 ? 0 : T.m_end[lb + q0 - 1];
-        for (int i = lane; i < nmem; i += 32) {
-          S.sbeg[i] = T.m_sb[lb + q0 + i];
-          S.pref[i + 1] = T.m_end[lb + q0 + i] - base;
-        }
-        if (lane == 0) S.pref[0] = 0;
+      for (int i = lane; i < nmem; i += 32) {  // expand the members overlapping the window
+        const int pa = S.pref[i], pe = S.pref[i + 1];
+        const int a = pa > w0 ? pa : w0, e = pe < w0 + wn ? pe : w0 + wn;
+        const int sb = S.sbeg[i] - pa;
+        for (int j = a; j < e; j++) S.map[j - w0] = sb + j;
       }
-      __syncwarp();
-      const int total = S.pref[nmem];
-      int cur = 0;  // member cursor (slots visited in increasing order)
-      for (int pb = 0; pb < total; pb += 32 * RS) {
-        double y[RS][D], yy[RS], qs[RS], col[RS];
-        int64_t gidx[RS];
-        bool ok[RS];
-#pragma unroll
-        for (int s = 0; s < RS; s++) {
-          int j = pb + lane + 32 * s;
-          ok[s] = j < total;
-          if (!ok[s]) j = pb;  // dummy slot: a copy of the pass's first source with zero charge
-          int c = ok[s] ? cur : 0;
-          while (S.pref[c + 1] <= j) c++;
-          if (ok[s]) cur = c;
-          gidx[s] = (int64_t)S.sbeg[c] + (j - S.pref[c]);
-          double yv[D], q;
-          load_rec<D>(T.rec, gidx[s], yv, q);
+      for (int tc0 = 0; tc0 < m; tc0 += TB) {
+        const int tcnt = m - tc0 < TB ? m - tc0 : TB;
+        const int tpad = (tcnt + 1) & ~1;
+        __syncwarp();
+        if (lane < tpad) {  // stage this chunk's targets (an odd count gets a zero-charge copy of the first)
+          double x[D], q;
+          load_rec<D>(T.rec, tb + tc0 + (lane < tcnt ? lane : 0), x, q);
+          double* v = S.tgt[lane].v;
           double n2 = 0.0;
 #pragma unroll
           for (int k = 0; k < D; k++) {
-            y[s][k] = yv[k] - o[k];
-            n2 = fma(y[s][k], y[s][k], n2);
+            const double dk = x[k] - o[k];
+            n2 = fma(dk, dk, n2);
+            v[k] = MODE == SYM_M2L ? -2.0 * dk : dk;
           }
-          yy[s] = n2;
-          qs[s] = ok[s] ? q : 0.0;
-          col[s] = 0.0;
+          v[D] = n2;
+          v[D + 1] = lane < tcnt ? q : 0.0;
         }
+        __syncwarp();
+        double p[TB];
 #pragma unroll
-        for (int t = 0; t < TB; t++) {
-          if (t >= tcnt) break;
-          double a[NV];
-#pragma unroll
-          for (int i = 0; i < NV; i += 2) {
-            const double2 u = *reinterpret_cast<const double2*>(&S.tgt[t].v[i]);
-            a[i] = u.x;
-            a[i + 1] = u.y;
-          }
+        for (int t = 0; t < TB; t++) p[t] = 0.0;
+        for (int pb = 0; pb < wn; pb += 32 * RS) {
+          double y[RS][D], yy[RS], qs[RS], col[RS];
+          int gidx[RS];
 #pragma unroll
           for (int s = 0; s < RS; s++) {
-            double r2;
-            if constexpr (MODE == SYM_M2L) {
-              r2 = a[D] + yy[s];
+            const int j = pb + lane + 32 * s;
+            const bool ok = j < wn;
+            gidx[s] = S.map[ok ? j : pb];  // dummy slot: a copy of the pass's first source with zero charge
+            double yv[D], q;
+            load_rec<D>(T.rec, gidx[s], yv, q);
+            double n2 = 0.0;
 #pragma unroll
-              for (int k = 0; k < D; k++) r2 = fma(a[k], y[s][k], r2);
-            } else {
-              r2 = 0.0;
-#pragma unroll
-              for (int k = 0; k < D; k++) {
-                const double dk = a[k] - y[s][k];
-                r2 = fma(dk, dk, r2);
-              }
+            for (int k = 0; k < D; k++) {
+              y[s][k] = yv[k] - o[k];
+              n2 = fma(y[s][k], y[s][k], n2);
             }
-            const double kv = sym_kval<KIND, MODE, F32S>(r2, kp);
-            if constexpr (MODE != SYM_SELF) col[s] = fma(kv, a[D + 1], col[s]);
-            p[t] = fma(kv, qs[s], p[t]);
+            yy[s] = n2;
+            qs[s] = ok ? q : 0.0;
+            col[s] = 0.0;
+            if (!ok) gidx[s] = -1;
+          }
+#pragma unroll
+          for (int t = 0; t < TB; t += 2) {
+            if (t >= tpad) break;
+            double a0[NV], a1[NV];
+            load_tgt<D>(S, t, a0);
+            load_tgt<D>(S, t + 1, a1);
+#pragma unroll
+            for (int s = 0; s < RS; s++) sym_pair<D, KIND, MODE, F32S, NV>(a0, y[s], yy[s], qs[s], col[s], p[t], kp);
+#pragma unroll
+            for (int s = 0; s < RS; s++)
+              sym_pair<D, KIND, MODE, F32S, NV>(a1, y[s], yy[s], qs[s], col[s], p[t + 1], kp);
+          }
+          if constexpr (MODE != SYM_SELF) {
+#pragma unroll
+            for (int s = 0; s < RS; s++)
+              if (gidx[s] >= 0) atomicAdd(T.out + (int64_t)gidx[s] * R + r0, col[s] * SCALE);
           }
         }
-        if constexpr (MODE != SYM_SELF) {
-#pragma unroll
-          for (int s = 0; s < RS; s++)
-            if (ok[s]) atomicAdd(T.out + gidx[s] * R + r0, col[s] * SCALE);
-        }
+        const double tot = warp_reduce_scatter16(p, lane);
+        const int t = lane >> 1;
+        if ((lane & 1) == 0 && t < tcnt) atomicAdd(T.out + (int64_t)(tb + tc0 + t) * R + r0, tot * SCALE);
       }
     }
-    // reduce the TB row partials over the warp: reduce-scatter (lane >> 1 ends up holding target lane >> 1 for
-    // TB = 16), then add into the targets' rows
-    static_assert(TB == 16, "reduce-scatter written for TB = 16");
-    double v8[8], v4[4], v2[2], v1;
-    {
-      const bool hi = lane & 16;
-#pragma unroll
-      for (int i = 0; i < 8; i++) {
-        const double send = hi ? p[i] : p[i + 8];
-        const double keep = hi ? p[i + 8] : p[i];
-        v8[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-      }
-    }
-    {
-      const bool hi = lane & 8;
-#pragma unroll
-      for (int i = 0; i < 4; i++) {
-        const double send = hi ? v8[i] : v8[i + 4];
-        const double keep = hi ? v8[i + 4] : v8[i];
-        v4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-      }
-    }
-    {
-      const bool hi = lane & 4;
-#pragma unroll
-      for (int i = 0; i < 2; i++) {
-        const double send = hi ? v4[i] : v4[i + 2];
-        const double keep = hi ? v4[i + 2] : v4[i];
-        v2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-      }
-    }
-    {
-      const bool hi = lane & 2;
-      const double send = hi ? v2[0] : v2[1];
-      const double keep = hi ? v2[1] : v2[0];
-      v1 = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-    }
-    v1 += __shfl_xor_sync(0xffffffffu, v1, 1);
-    const int t = lane >> 1;
-    if ((lane & 1) == 0 && t < tcnt) atomicAdd(T.out + (int64_t)(tb + tc0 + t) * R + r0, v1 * SCALE);
   }
 }
 

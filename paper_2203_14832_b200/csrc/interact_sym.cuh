@@ -73,10 +73,20 @@ constexpr int SYM_MAP = H2B_SYM_MAP;  // slots of a source window (record indice
 template <int D>
 struct alignas(16) SymWarp {
   SymTgt<D> tgt[H2B_SYM_TB];
+  double2 rbuf[2][32 * H2B_SYM_RS * SrcRec<D, 1>::W];  // source records of the current / next pass (cp.async)
   int pref[SYM_MAXMEM + 1];
   int sbeg[SYM_MAXMEM];
   int map[SYM_MAP];  // window slot -> record index
 };
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
 template <int D>
 __device__ __forceinline__ void load_rec(const double2* rec, int64_t i, double (&y)[D], double& q) {
@@ -257,26 +267,52 @@ __device__ __forceinline__ void sym_item(const SymTab& T, int4 dsc, int64_t R, i
         double p[TB];
 #pragma unroll
         for (int t = 0; t < TB; t++) p[t] = 0.0;
-        for (int pb = 0; pb < wn; pb += 32 * RS) {
-          double y[RS][D], yy[RS], qs[RS], col[RS];
-          int gidx[RS];
+        // passes of 32 RS slots; each lane copies its own slots' records for the next pass (cp.async) while the
+        // current one computes, and reads back only what it copied itself (no cross-lane synchronisation)
+        constexpr int W = SrcRec<D, 1>::W;
+        int gnext[RS];
+        auto issue = [&](int pb, int buf) {
 #pragma unroll
           for (int s = 0; s < RS; s++) {
             const int j = pb + lane + 32 * s;
-            const bool ok = j < wn;
-            gidx[s] = S.map[ok ? j : pb];  // dummy slot: a copy of the pass's first source with zero charge
-            double yv[D], q;
-            load_rec<D>(T.rec, gidx[s], yv, q);
+            gnext[s] = j < wn ? S.map[j] : -1;
+            const int g = S.map[j < wn ? j : pb];  // dummy slot: a copy of the pass's first source
+#pragma unroll
+            for (int w = 0; w < W; w++) cp_async16(&S.rbuf[buf][(lane + 32 * s) * W + w], T.rec + (int64_t)g * W + w);
+          }
+          cp_async_commit();
+        };
+        issue(0, 0);
+        int pi = 0;
+        for (int pb = 0; pb < wn; pb += 32 * RS, pi ^= 1) {
+          int gidx[RS];
+#pragma unroll
+          for (int s = 0; s < RS; s++) gidx[s] = gnext[s];
+          if (pb + 32 * RS < wn) {
+            issue(pb + 32 * RS, pi ^ 1);
+            cp_async_wait<1>();
+          } else {
+            cp_async_wait<0>();
+          }
+          double y[RS][D], yy[RS], qs[RS], col[RS];
+#pragma unroll
+          for (int s = 0; s < RS; s++) {
+            double v[2 * W];
+#pragma unroll
+            for (int w = 0; w < W; w++) {
+              const double2 u = S.rbuf[pi][(lane + 32 * s) * W + w];
+              v[2 * w] = u.x;
+              v[2 * w + 1] = u.y;
+            }
             double n2 = 0.0;
 #pragma unroll
             for (int k = 0; k < D; k++) {
-              y[s][k] = yv[k] - o[k];
+              y[s][k] = v[k] - o[k];
               n2 = fma(y[s][k], y[s][k], n2);
             }
             yy[s] = n2;
-            qs[s] = ok ? q : 0.0;
+            qs[s] = gidx[s] >= 0 ? v[D] : 0.0;
             col[s] = 0.0;
-            if (!ok) gidx[s] = -1;
           }
 #pragma unroll
           for (int t = 0; t < TB; t += 2) {
@@ -310,12 +346,13 @@ __global__ void __launch_bounds__(SYM_THREADS, H2B_SYM_MINB)
     interact_sym(const int64_t* __restrict__ items, const int4* __restrict__ descs, int64_t n_items,
                  unsigned long long* __restrict__ counter, const SymTab* __restrict__ tabs, int ntabs, int near_list,
                  int self_list, int64_t R, int64_t r0, KParams kp) {
-  __shared__ SymTab tab_s[32];
-  __shared__ SymWarp<D> ws[SYM_THREADS / 32];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  SymTab* tab_s = reinterpret_cast<SymTab*>(smem_raw);
+  const size_t tab_bytes = (sizeof(SymTab) * ntabs + 127) / 128 * 128;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < ntabs; i += blockDim.x) tab_s[i] = tabs[i];
   __syncthreads();
-  SymWarp<D>& S = ws[warp];
+  SymWarp<D>& S = reinterpret_cast<SymWarp<D>*>(smem_raw + tab_bytes)[warp];
   for (;;) {
     unsigned long long idx = 0;
     if (lane == 0) idx = atomicAdd(counter, 1ull);
@@ -341,7 +378,10 @@ void launch_sym(const DevH2& h, int64_t R, int64_t r0, const KParams& kp, cudaSt
   int dev = 0, nsm = 0, per = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, SYM_THREADS, 0));
+  const int ntabs = L + 3;
+  const size_t smem = (sizeof(SymTab) * ntabs + 127) / 128 * 128 + (SYM_THREADS / 32) * sizeof(SymWarp<D>);
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, SYM_THREADS, smem));
   const int64_t grid = std::min<int64_t>((int64_t)nsm * std::max(per, 1),
                                          (h.n_sym_items + SYM_THREADS / 32 - 1) / (SYM_THREADS / 32));
   // one RHS of a wider product: pack this column's charges into the records (the gather / upward pass wrote
@@ -353,9 +393,9 @@ void launch_sym(const DevH2& h, int64_t R, int64_t r0, const KParams& kp, cudaSt
     CKL();
   }
   CK(cudaMemsetAsync(h.work_counter.get(), 0, sizeof(unsigned long long), s));
-  kern<<<(unsigned)grid, SYM_THREADS, 0, s>>>(h.sym_items.get(), reinterpret_cast<const int4*>(h.sym_desc.get()),
+  kern<<<(unsigned)grid, SYM_THREADS, smem, s>>>(h.sym_items.get(), reinterpret_cast<const int4*>(h.sym_desc.get()),
                                               h.n_sym_items, h.work_counter.get(),
-                                              reinterpret_cast<const SymTab*>(h.sym_tabs.get()), L + 3, L + 1, L + 2,
+                                              reinterpret_cast<const SymTab*>(h.sym_tabs.get()), ntabs, L + 1, L + 2,
                                               R, r0, kp);
   CKL();
 }

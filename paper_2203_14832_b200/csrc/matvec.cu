@@ -384,7 +384,7 @@ __global__ void item_costs(int64_t n, int lev, const int64_t* __restrict__ t_ptr
 }
 
 // symmetric kernel work items: (list, cell) with cost = targets x upper-partner sources (self block: m^2)
-__global__ void sym_costs(int64_t n, int lst, int self, const int64_t* __restrict__ ptr,
+__global__ void sym_costs(int64_t n, int lst, int self, int lst_is_near, const int64_t* __restrict__ ptr,
                           const int64_t* __restrict__ l_ptr, const int64_t* __restrict__ l_idx,
                           unsigned long long* __restrict__ cost, int64_t* __restrict__ item) {
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -399,7 +399,10 @@ __global__ void sym_costs(int64_t n, int lst, int self, const int64_t* __restric
       if (y > c) src += ptr[y + 1] - ptr[y];
     }
   }
-  cost[c] = (m > 0 && src > 0) ? (unsigned long long)(m * src) + 1ull : 0ull;
+  // sorted descending: M2L items first, then near field, then self blocks (warps of an SM then mostly run one
+  // code path at a time: the three item kinds together overflow the instruction cache), each by pair count
+  const unsigned long long band = self ? 0ull : (l_ptr && lst_is_near ? 1ull : 2ull);
+  cost[c] = (m > 0 && src > 0) ? (band << 56) | ((unsigned long long)(m * src) + 1ull) : 0ull;
   item[c] = ((int64_t)lst << 40) | c;
 }
 
@@ -525,14 +528,14 @@ void build_sym(DevH2& h, cudaStream_t s) {
     const bool nf = l == L + 1;
     const DevLevel& Lv = T.lv[nf ? L : l];
     if (Lv.n)
-      sym_costs<<<nblk(Lv.n, 256), 256, 0, s>>>(Lv.n, l, 0, sb[l].ptr, sb[l].l_ptr,
+      sym_costs<<<nblk(Lv.n, 256), 256, 0, s>>>(Lv.n, l, 0, nf ? 1 : 0, sb[l].ptr, sb[l].l_ptr,
                                                 nf ? Lv.nb_idx.get() : Lv.il_idx.get(), cost.get() + off,
                                                 item.get() + off);
     CKL();
     off += Lv.n;
   }
   if (T.lv[L].n)
-    sym_costs<<<nblk(T.lv[L].n, 256), 256, 0, s>>>(T.lv[L].n, L + 2, 1, sb[L + 2].ptr, nullptr, nullptr,
+    sym_costs<<<nblk(T.lv[L].n, 256), 256, 0, s>>>(T.lv[L].n, L + 2, 1, 0, sb[L + 2].ptr, nullptr, nullptr,
                                                    cost.get() + off, item.get() + off);
   CKL();
   size_t bytes = 0;

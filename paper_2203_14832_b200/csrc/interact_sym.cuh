@@ -13,9 +13,9 @@
 // which halves the kernel evaluations (r^2 + rsqrt + Newton) per product.
 //
 // Work item = (list, cell X): list l in [2, L] is level l's interaction list,
-// L + 1 the leaf near field (neighbour leaves Y > X, difference-form r^2),
-// L + 2 the leaf self block K(X, X) (row sums only, r2 == 0 -> 0, the
-// punctured diagonal).  One warp per item.  X's targets are staged TB at a
+// L + 1 the leaf near field: neighbour leaves Y > X plus X itself, whose
+// block K(X, X) is evaluated in both orders with row sums only (r2 == 0 ->
+// 0, the punctured diagonal); difference-form r^2.  One warp per item.  X's targets are staged TB at a
 // time in the warp's shared memory and broadcast; the "upper" partners'
 // source records (contiguous Morton ranges, adjacent ones merged) are spread
 // over the lanes, RS records per lane held in registers with their column
@@ -30,6 +30,8 @@
 // pass.  Both go to the level's u_in (and the near-field buffer) with FP64
 // reductions (RED.ADD.F64), so those buffers are zeroed first.
 #pragma once
+#include <climits>
+
 #include "interact.cuh"
 
 namespace h2b {
@@ -56,7 +58,7 @@ struct SymTab {
   double* out;         // result rows (record index) * R + r0
 };
 
-enum SymMode { SYM_M2L = 0, SYM_NEAR = 1, SYM_SELF = 2 };
+enum SymMode { SYM_M2L = 0, SYM_NEAR = 1 };
 
 template <int D>
 struct alignas(16) SymTgt {  // one staged target: M2L a = (-2 x', |x'|^2), near a = x'
@@ -107,22 +109,21 @@ __device__ __forceinline__ void load_rec(const double2* rec, int64_t i, double (
 template <int KIND, int MODE, bool F32S>
 __device__ __forceinline__ double sym_kval(double r2, const KParams& kp) {
   if constexpr (is_inv_r<KIND>()) {
-    if constexpr (MODE == SYM_SELF) {
-      const bool zero = __double2hiint(r2) == 0;  // r2 == 0 (or subnormal): the punctured diagonal
+    if constexpr (MODE == SYM_NEAR) {
+      // near field (plain input charges): FP64 seed + quadratic step; the item's own leaf is among the sources,
+      // so r2 == 0 (a point with itself or a duplicate) gives 0, the punctured diagonal
+      const bool zero = __double2hiint(r2) == 0;  // r2 == 0 (or subnormal)
       const double r2s = zero ? 1.0 : r2;
       const double y = rsq_approx(r2s);
       const double kv = y * fma(-r2s, y * y, 3.0);
       return zero ? 0.0 : kv;
-    } else if constexpr (MODE == SYM_M2L && F32S) {
+    } else if constexpr (F32S) {
       const double y = rsq_seed_f32(r2);  // FP32 seed + quadratic step (interact.cuh rsq_seed_f32)
       return y * fma(-r2, y * y, 3.0);
-    } else if constexpr (MODE == SYM_M2L) {
+    } else {
       const double y = rsq_approx(r2);  // FP64 seed + cubic step (multipole charges amplify a bias)
       const double e = fma(-r2, y * y, 1.0);
       return y * fma(e, fma(0.75, e, 1.0), 2.0);
-    } else {  // near field between distinct leaves: r2 > 0, plain input charges
-      const double y = rsq_approx(r2);
-      return y * fma(-r2, y * y, 3.0);
     }
   } else {
     return kfast<KIND>(r2, kp);
@@ -183,7 +184,7 @@ __device__ __forceinline__ void sym_pair(const double (&a)[NV], const double (&y
     }
   }
   const double kv = sym_kval<KIND, MODE, F32S>(r2, kp);
-  if constexpr (MODE != SYM_SELF) col = fma(kv, a[D + 1], col);
+  col = fma(kv, a[D + 1], col);
   p = fma(kv, qs, p);
 }
 
@@ -213,24 +214,26 @@ __device__ __forceinline__ void sym_item(const SymTab& T, int4 dsc, int64_t R, i
     double q;
     load_rec<D>(T.rec, tb, o, q);
   }
-  const int nchunk_m = MODE == SYM_SELF ? 1 : (cnt + SYM_MAXMEM - 1) / SYM_MAXMEM;
-  for (int mc = 0; mc < nchunk_m; mc++) {
-    int nmem;
+  // virtual member list: near field = [the leaf itself (row sums only: both orders of each pair inside the
+  // block are evaluated), upper neighbours]; M2L = [upper interaction-list cells]
+  constexpr int SELF0 = MODE == SYM_NEAR ? 1 : 0;
+  const int vc = cnt + SELF0;
+  for (int v0 = 0; v0 < vc; v0 += SYM_MAXMEM) {
+    const int nmem = vc - v0 < SYM_MAXMEM ? vc - v0 : SYM_MAXMEM;
     __syncwarp();
-    if constexpr (MODE == SYM_SELF) {  // the cell itself
-      nmem = 1;
-      if (lane == 0) {
-        S.sbeg[0] = tb;
-        S.pref[0] = 0;
-        S.pref[1] = m;
-      }
-    } else {
-      const int q0 = mc * SYM_MAXMEM;
-      nmem = cnt - q0 < SYM_MAXMEM ? cnt - q0 : SYM_MAXMEM;
-      const int base = q0 == 0 ? 0 : T.m_end[lb + q0 - 1];
+    {
+      const int r0m = v0 - SELF0;  // real member index of virtual index v0
+      const int base = r0m <= 0 ? 0 : T.m_end[lb + r0m - 1];
+      const int selfn = (SELF0 && v0 == 0) ? m : 0;
       for (int i = lane; i < nmem; i += 32) {
-        S.sbeg[i] = T.m_sb[lb + q0 + i];
-        S.pref[i + 1] = T.m_end[lb + q0 + i] - base;
+        const int r = r0m + i;
+        if (r < 0) {
+          S.sbeg[i] = -(tb + 1);  // row-only member: the item's own leaf
+          S.pref[i + 1] = m;
+        } else {
+          S.sbeg[i] = T.m_sb[lb + r];
+          S.pref[i + 1] = selfn + T.m_end[lb + r] - base;
+        }
       }
       if (lane == 0) S.pref[0] = 0;
     }
@@ -242,8 +245,12 @@ __device__ __forceinline__ void sym_item(const SymTab& T, int4 dsc, int64_t R, i
       for (int i = lane; i < nmem; i += 32) {  // expand the members overlapping the window
         const int pa = S.pref[i], pe = S.pref[i + 1];
         const int a = pa > w0 ? pa : w0, e = pe < w0 + wn ? pe : w0 + wn;
-        const int sb = S.sbeg[i] - pa;
-        for (int j = a; j < e; j++) S.map[j - w0] = sb + j;
+        const int sg = S.sbeg[i];
+        if (sg >= 0) {
+          for (int j = a; j < e; j++) S.map[j - w0] = sg + (j - pa);
+        } else {  // row-only records are stored as -(index + 1)
+          for (int j = a; j < e; j++) S.map[j - w0] = sg - (j - pa);
+        }
       }
       for (int tc0 = 0; tc0 < m; tc0 += TB) {
         const int tcnt = m - tc0 < TB ? m - tc0 : TB;
@@ -275,8 +282,9 @@ __device__ __forceinline__ void sym_item(const SymTab& T, int4 dsc, int64_t R, i
 #pragma unroll
           for (int s = 0; s < RS; s++) {
             const int j = pb + lane + 32 * s;
-            gnext[s] = j < wn ? S.map[j] : -1;
-            const int g = S.map[j < wn ? j : pb];  // dummy slot: a copy of the pass's first source
+            const int g0 = S.map[j < wn ? j : pb];  // dummy slot: a copy of the pass's first source
+            gnext[s] = j < wn ? g0 : INT_MIN;
+            const int g = g0 >= 0 ? g0 : -g0 - 1;
 #pragma unroll
             for (int w = 0; w < W; w++) cp_async16(&S.rbuf[buf][(lane + 32 * s) * W + w], T.rec + (int64_t)g * W + w);
           }
@@ -311,7 +319,7 @@ __device__ __forceinline__ void sym_item(const SymTab& T, int4 dsc, int64_t R, i
               n2 = fma(y[s][k], y[s][k], n2);
             }
             yy[s] = n2;
-            qs[s] = gidx[s] >= 0 ? v[D] : 0.0;
+            qs[s] = gidx[s] != INT_MIN ? v[D] : 0.0;
             col[s] = 0.0;
           }
 #pragma unroll
@@ -326,11 +334,9 @@ __device__ __forceinline__ void sym_item(const SymTab& T, int4 dsc, int64_t R, i
             for (int s = 0; s < RS; s++)
               sym_pair<D, KIND, MODE, F32S, NV>(a1, y[s], yy[s], qs[s], col[s], p[t + 1], kp);
           }
-          if constexpr (MODE != SYM_SELF) {
 #pragma unroll
-            for (int s = 0; s < RS; s++)
-              if (gidx[s] >= 0) atomicAdd(T.out + (int64_t)gidx[s] * R + r0, col[s] * SCALE);
-          }
+          for (int s = 0; s < RS; s++)
+            if (gidx[s] >= 0) atomicAdd(T.out + (int64_t)gidx[s] * R + r0, col[s] * SCALE);
         }
         const double tot = warp_reduce_scatter16(p, lane);
         const int t = lane >> 1;
@@ -345,7 +351,7 @@ template <int D, int KIND, int RS, int TB, bool F32S>
 __global__ void __launch_bounds__(SYM_THREADS, H2B_SYM_MINB)
     interact_sym(const int64_t* __restrict__ items, const int4* __restrict__ descs, int64_t n_items,
                  unsigned long long* __restrict__ counter, const SymTab* __restrict__ tabs, int ntabs, int near_list,
-                 int self_list, int64_t R, int64_t r0, KParams kp) {
+                 int64_t R, int64_t r0, KParams kp) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SymTab* tab_s = reinterpret_cast<SymTab*>(smem_raw);
   const size_t tab_bytes = (sizeof(SymTab) * ntabs + 127) / 128 * 128;
@@ -361,9 +367,7 @@ __global__ void __launch_bounds__(SYM_THREADS, H2B_SYM_MINB)
     const int lst = (int)(items[idx] >> 40);
     const int4 dsc = descs[idx];
     const SymTab& T = tab_s[lst];
-    if (lst == self_list)
-      sym_item<D, KIND, RS, TB, F32S, SYM_SELF>(T, dsc, R, r0, kp, S);
-    else if (lst == near_list)
+    if (lst == near_list)
       sym_item<D, KIND, RS, TB, F32S, SYM_NEAR>(T, dsc, R, r0, kp, S);
     else
       sym_item<D, KIND, RS, TB, F32S, SYM_M2L>(T, dsc, R, r0, kp, S);
@@ -378,7 +382,7 @@ void launch_sym(const DevH2& h, int64_t R, int64_t r0, const KParams& kp, cudaSt
   int dev = 0, nsm = 0, per = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  const int ntabs = L + 3;
+  const int ntabs = L + 2;
   const size_t smem = (sizeof(SymTab) * ntabs + 127) / 128 * 128 + (SYM_THREADS / 32) * sizeof(SymWarp<D>);
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, SYM_THREADS, smem));
@@ -395,7 +399,7 @@ void launch_sym(const DevH2& h, int64_t R, int64_t r0, const KParams& kp, cudaSt
   CK(cudaMemsetAsync(h.work_counter.get(), 0, sizeof(unsigned long long), s));
   kern<<<(unsigned)grid, SYM_THREADS, smem, s>>>(h.sym_items.get(), reinterpret_cast<const int4*>(h.sym_desc.get()),
                                               h.n_sym_items, h.work_counter.get(),
-                                              reinterpret_cast<const SymTab*>(h.sym_tabs.get()), ntabs, L + 1, L + 2,
+                                              reinterpret_cast<const SymTab*>(h.sym_tabs.get()), ntabs, L + 1,
                                               R, r0, kp);
   CKL();
 }

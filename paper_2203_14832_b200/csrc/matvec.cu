@@ -383,25 +383,22 @@ __global__ void item_costs(int64_t n, int lev, const int64_t* __restrict__ t_ptr
   item[c] = ((int64_t)lev << 40) | c;
 }
 
-// symmetric kernel work items: (list, cell) with cost = targets x upper-partner sources (self block: m^2)
-__global__ void sym_costs(int64_t n, int lst, int self, int lst_is_near, const int64_t* __restrict__ ptr,
+// symmetric kernel work items: (list, cell) with cost = targets x upper-partner sources (near field: plus the
+// leaf's own block)
+__global__ void sym_costs(int64_t n, int lst, int near, const int64_t* __restrict__ ptr,
                           const int64_t* __restrict__ l_ptr, const int64_t* __restrict__ l_idx,
                           unsigned long long* __restrict__ cost, int64_t* __restrict__ item) {
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= n) return;
   const int64_t m = ptr[c + 1] - ptr[c];
-  int64_t src = 0;
-  if (self) {
-    src = m;
-  } else {
-    for (int64_t q = l_ptr[c]; q < l_ptr[c + 1]; q++) {
-      const int64_t y = l_idx[q];
-      if (y > c) src += ptr[y + 1] - ptr[y];
-    }
+  int64_t src = near ? m : 0;
+  for (int64_t q = l_ptr[c]; q < l_ptr[c + 1]; q++) {
+    const int64_t y = l_idx[q];
+    if (y > c) src += ptr[y + 1] - ptr[y];
   }
-  // sorted descending: M2L items first, then near field, then self blocks (warps of an SM then mostly run one
-  // code path at a time: the three item kinds together overflow the instruction cache), each by pair count
-  const unsigned long long band = self ? 0ull : (l_ptr && lst_is_near ? 1ull : 2ull);
+  // sorted descending: M2L items first, then the near field (warps of an SM then mostly run one code path at a
+  // time: both together overflow the instruction cache), each by pair count
+  const unsigned long long band = near ? 1ull : 2ull;
   cost[c] = (m > 0 && src > 0) ? (band << 56) | ((unsigned long long)(m * src) + 1ull) : 0ull;
   item[c] = ((int64_t)lst << 40) | c;
 }
@@ -413,7 +410,7 @@ struct SymBuild {
 };
 
 __global__ void make_sym_desc(const int64_t* __restrict__ items, int64_t n, const SymBuild* __restrict__ sb,
-                              int self_list, int4* __restrict__ desc) {
+                              int4* __restrict__ desc) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int64_t it = items[i];
@@ -421,8 +418,7 @@ __global__ void make_sym_desc(const int64_t* __restrict__ items, int64_t n, cons
   const int64_t c = it & ((1ll << 40) - 1);
   const SymBuild& B = sb[lst];
   const int64_t tb = B.ptr[c];
-  const bool self = lst == self_list;
-  desc[i] = make_int4((int)tb, (int)(B.ptr[c + 1] - tb), self ? 0 : (int)B.l_ptr[c], self ? 0 : B.u_cnt[c]);
+  desc[i] = make_int4((int)tb, (int)(B.ptr[c + 1] - tb), (int)B.l_ptr[c], B.u_cnt[c]);
 }
 
 KParams make_kp(int kind, double a) {
@@ -481,17 +477,17 @@ void build_items(DevH2& h, cudaStream_t s) {
 }
 
 // Symmetric kernel (interact_sym.cuh): upper member tables, work items by descending pair count and their
-// descriptors.  Static per H2 matrix.  List ids: 2..L = M2L levels, L + 1 = near field, L + 2 = self blocks.
+// descriptors.  Static per H2 matrix.  List ids: 2..L = M2L levels, L + 1 = near field.
 void build_sym(DevH2& h, cudaStream_t s) {
   const DevTree& T = *h.t;
   const int L = T.depth;
   h.u_sb.clear();
   h.u_end.clear();
   h.u_cnt.clear();
-  h.u_sb.resize(L + 3);
-  h.u_end.resize(L + 3);
-  h.u_cnt.resize(L + 3);
-  std::vector<SymBuild> sb(L + 3);
+  h.u_sb.resize(L + 2);
+  h.u_end.resize(L + 2);
+  h.u_cnt.resize(L + 2);
+  std::vector<SymBuild> sb(L + 2);
   std::memset(sb.data(), 0, sizeof(SymBuild) * sb.size());
   std::vector<int> ids;
   for (int l = 2; l <= L; l++) ids.push_back(l);
@@ -513,9 +509,8 @@ void build_sym(DevH2& h, cudaStream_t s) {
     sb[l].l_ptr = nf ? Lv.nb_ptr.get() : Lv.il_ptr.get();
     sb[l].u_cnt = h.u_cnt[l].get();
   }
-  sb[L + 2].ptr = T.lv[L].t_ptr.get();
   // items
-  int64_t total = 2 * T.lv[L].n;
+  int64_t total = T.lv[L].n;
   for (int l = 2; l <= L; l++) total += T.lv[l].n;
   DBuf<unsigned long long> cost, cost_sorted;
   DBuf<int64_t> item;
@@ -528,16 +523,12 @@ void build_sym(DevH2& h, cudaStream_t s) {
     const bool nf = l == L + 1;
     const DevLevel& Lv = T.lv[nf ? L : l];
     if (Lv.n)
-      sym_costs<<<nblk(Lv.n, 256), 256, 0, s>>>(Lv.n, l, 0, nf ? 1 : 0, sb[l].ptr, sb[l].l_ptr,
+      sym_costs<<<nblk(Lv.n, 256), 256, 0, s>>>(Lv.n, l, nf ? 1 : 0, sb[l].ptr, sb[l].l_ptr,
                                                 nf ? Lv.nb_idx.get() : Lv.il_idx.get(), cost.get() + off,
                                                 item.get() + off);
     CKL();
     off += Lv.n;
   }
-  if (T.lv[L].n)
-    sym_costs<<<nblk(T.lv[L].n, 256), 256, 0, s>>>(T.lv[L].n, L + 2, 1, 0, sb[L + 2].ptr, nullptr, nullptr,
-                                                   cost.get() + off, item.get() + off);
-  CKL();
   size_t bytes = 0;
   CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, cost.get(), cost_sorted.get(), item.get(),
                                                h.sym_items.get(), total, 0, 64, s));
@@ -554,7 +545,7 @@ void build_sym(DevH2& h, cudaStream_t s) {
   CK(cudaMemcpyAsync(dsb.get(), sb.data(), sizeof(SymBuild) * sb.size(), cudaMemcpyHostToDevice, s));
   h.sym_desc.alloc(4 * std::max<int64_t>(nz, 1), &h.mem);
   if (nz)
-    make_sym_desc<<<nblk(nz, 256), 256, 0, s>>>(h.sym_items.get(), nz, dsb.get(), L + 2,
+    make_sym_desc<<<nblk(nz, 256), 256, 0, s>>>(h.sym_items.get(), nz, dsb.get(),
                                                 reinterpret_cast<int4*>(h.sym_desc.get()));
   CKL();
   CK(cudaStreamSynchronize(s));
@@ -565,17 +556,18 @@ void build_sym(DevH2& h, cudaStream_t s) {
 void build_sym_tabs(DevH2& h, cudaStream_t s) {
   const DevTree& T = *h.t;
   const int L = T.depth;
-  std::vector<SymTab> tabs(L + 3);
+  std::vector<SymTab> tabs(L + 2);
   std::memset(tabs.data(), 0, sizeof(SymTab) * tabs.size());
-  for (int l = 2; l <= L + 2; l++) {
+  std::vector<int> ids;
+  for (int l = 2; l <= L; l++) ids.push_back(l);
+  ids.push_back(L + 1);  // the near field (also when the tree has fewer than two levels)
+  for (int l : ids) {
     SymTab& t = tabs[l];
     const bool leaf = l > L;
     t.rec = h.pack1.lists[leaf ? std::max(L - 1, 0) : l - 2].get();
     t.ptr = leaf ? T.lv[L].t_ptr.get() : h.lv[l].in_ptr.get();
-    if (l <= L + 1) {
-      t.m_sb = h.u_sb[l].get();
-      t.m_end = h.u_end[l].get();
-    }
+    t.m_sb = h.u_sb[l].get();
+    t.m_end = h.u_end[l].get();
     t.out = leaf ? h.near.get() : h.uin[l].get();
   }
   h.sym_tabs.alloc(sizeof(SymTab) * tabs.size(), &h.mem);

@@ -110,6 +110,7 @@ struct DevH2 {
   DBuf<int64_t> sym_items;
   DBuf<int> sym_desc;
   int64_t n_sym_items = 0;
+  bool sym_wide = false;  // 32-target chunks (most pairs in items with > 16 targets) instead of 16
   DBuf<unsigned char> sym_tabs;
   bool sym_ready = false;
 };

@@ -38,14 +38,10 @@ namespace h2b {
 namespace {
 
 #ifndef H2B_SYM_RS
-#define H2B_SYM_RS 3
+#define H2B_SYM_RS 2
 #endif
-#ifndef H2B_SYM_TB
-#define H2B_SYM_TB 16
-#endif
-#ifndef H2B_SYM_MINB
-#define H2B_SYM_MINB 4
-#endif
+constexpr int SYM_NARROW = 16;  // target chunks of 16 (4 CTAs / SM, 128 registers) unless most pairs sit in items
+                                // with more targets: then chunks of 32 (fewer source passes), 3 CTAs / SM
 constexpr int SYM_THREADS = 128;
 constexpr int SYM_MAXMEM = 256;  // members staged per chunk of a cell's upper list
 
@@ -74,7 +70,7 @@ constexpr int SYM_MAP = H2B_SYM_MAP;  // slots of a source window (record indice
 
 template <int D>
 struct alignas(16) SymWarp {
-  SymTgt<D> tgt[H2B_SYM_TB];
+  SymTgt<D> tgt[32];
   double2 rbuf[2][32 * H2B_SYM_RS * SrcRec<D, 1>::W];  // source records of the current / next pass (cp.async)
   int pref[SYM_MAXMEM + 1];
   int sbeg[SYM_MAXMEM];
@@ -130,40 +126,28 @@ __device__ __forceinline__ double sym_kval(double r2, const KParams& kp) {
   }
 }
 
-// Sum of the TB = 16 row partials over the warp by a butterfly reduce-scatter: afterwards lanes 2t and
-// 2t + 1 hold the total of target t.
-__device__ __forceinline__ double warp_reduce_scatter16(const double (&p)[16], int lane) {
-  double v8[8], v4[4], v2[2];
-  {
-    const bool hi = lane & 16;
+// Sum of the TB (16 or 32) row partials over the warp by a butterfly reduce-scatter: afterwards lane l holds
+// the total of target l / (32 / TB).
+template <int TB>
+__device__ __forceinline__ double warp_reduce_scatter(const double (&p)[TB], int lane) {
+  static_assert(TB == 16 || TB == 32, "TB must be 16 or 32");
+  double v[TB];
 #pragma unroll
-    for (int i = 0; i < 8; i++) {
-      const double send = hi ? p[i] : p[i + 8];
-      const double keep = hi ? p[i + 8] : p[i];
-      v8[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  for (int i = 0; i < TB; i++) v[i] = p[i];
+#pragma unroll
+  for (int half = TB / 2, bit = 16; half >= 1; half /= 2, bit /= 2) {
+    const bool hi = lane & bit;
+#pragma unroll
+    for (int i = 0; i < half; i++) {
+      const double send = hi ? v[i] : v[i + half];
+      const double keep = hi ? v[i + half] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
     }
   }
-  {
-    const bool hi = lane & 8;
+  double r = v[0];
 #pragma unroll
-    for (int i = 0; i < 4; i++) {
-      const double send = hi ? v8[i] : v8[i + 4];
-      const double keep = hi ? v8[i + 4] : v8[i];
-      v4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-  }
-  {
-    const bool hi = lane & 4;
-#pragma unroll
-    for (int i = 0; i < 2; i++) {
-      const double send = hi ? v4[i] : v4[i + 2];
-      const double keep = hi ? v4[i + 2] : v4[i];
-      v2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-  }
-  const bool hi = lane & 2;
-  double v1 = (hi ? v2[1] : v2[0]) + __shfl_xor_sync(0xffffffffu, hi ? v2[0] : v2[1], 2);
-  return v1 + __shfl_xor_sync(0xffffffffu, v1, 1);
+  for (int bit = 32 / TB / 2; bit >= 1; bit /= 2) r += __shfl_xor_sync(0xffffffffu, r, bit);
+  return r;
 }
 
 // One pair: r^2, K, and both accumulations.
@@ -204,15 +188,16 @@ __device__ __forceinline__ void load_tgt(const SymWarp<D>& S, int t, double (&a)
 template <int D, int KIND, int RS, int TB, bool F32S, int MODE>
 __device__ __forceinline__ void sym_item(const SymTab& T, int4 dsc, int64_t R, int64_t r0, const KParams& kp,
                                          SymWarp<D>& S) {
-  static_assert(TB == 16, "reduce-scatter written for TB = 16");
   constexpr double SCALE = kscale<KIND>() * (is_inv_r<KIND>() ? 0.5 : 1.0);
   constexpr int NV = SymTgt<D>::N2;
   const int lane = threadIdx.x & 31;
   const int tb = dsc.x, m = dsc.y, lb = dsc.z, cnt = dsc.w;
+  const double2* rec = T.rec;  // in registers: the cp.async asm statements would force reloads from T
+  double* out = T.out;
   double o[D];  // frame origin: the item's first target
   {
     double q;
-    load_rec<D>(T.rec, tb, o, q);
+    load_rec<D>(rec, tb, o, q);
   }
   // virtual member list: near field = [the leaf itself (row sums only: both orders of each pair inside the
   // block are evaluated), upper neighbours]; M2L = [upper interaction-list cells]
@@ -258,7 +243,7 @@ __device__ __forceinline__ void sym_item(const SymTab& T, int4 dsc, int64_t R, i
         __syncwarp();
         if (lane < tpad) {  // stage this chunk's targets (an odd count gets a zero-charge copy of the first)
           double x[D], q;
-          load_rec<D>(T.rec, tb + tc0 + (lane < tcnt ? lane : 0), x, q);
+          load_rec<D>(rec, tb + tc0 + (lane < tcnt ? lane : 0), x, q);
           double* v = S.tgt[lane].v;
           double n2 = 0.0;
 #pragma unroll
@@ -286,7 +271,7 @@ __device__ __forceinline__ void sym_item(const SymTab& T, int4 dsc, int64_t R, i
             gnext[s] = j < wn ? g0 : INT_MIN;
             const int g = g0 >= 0 ? g0 : -g0 - 1;
 #pragma unroll
-            for (int w = 0; w < W; w++) cp_async16(&S.rbuf[buf][(lane + 32 * s) * W + w], T.rec + (int64_t)g * W + w);
+            for (int w = 0; w < W; w++) cp_async16(&S.rbuf[buf][(lane + 32 * s) * W + w], rec + (int64_t)g * W + w);
           }
           cp_async_commit();
         };
@@ -338,17 +323,18 @@ __device__ __forceinline__ void sym_item(const SymTab& T, int4 dsc, int64_t R, i
           for (int s = 0; s < RS; s++)
             if (gidx[s] >= 0) atomicAdd(T.out + (int64_t)gidx[s] * R + r0, col[s] * SCALE);
         }
-        const double tot = warp_reduce_scatter16(p, lane);
-        const int t = lane >> 1;
-        if ((lane & 1) == 0 && t < tcnt) atomicAdd(T.out + (int64_t)(tb + tc0 + t) * R + r0, tot * SCALE);
+        const double tot = warp_reduce_scatter<TB>(p, lane);
+        constexpr int LPT = 32 / TB;  // lanes per target after the reduce-scatter
+        const int t = lane / LPT;
+        if (lane % LPT == 0 && t < tcnt) atomicAdd(out + (int64_t)(tb + tc0 + t) * R + r0, tot * SCALE);
       }
     }
   }
 }
 
 // Persistent kernel: warps pull (list, cell) items by descending pair count.
-template <int D, int KIND, int RS, int TB, bool F32S>
-__global__ void __launch_bounds__(SYM_THREADS, H2B_SYM_MINB)
+template <int D, int KIND, int RS, int TB, int MINB, bool F32S>
+__global__ void __launch_bounds__(SYM_THREADS, MINB)
     interact_sym(const int64_t* __restrict__ items, const int4* __restrict__ descs, int64_t n_items,
                  unsigned long long* __restrict__ counter, const SymTab* __restrict__ tabs, int ntabs, int near_list,
                  int64_t R, int64_t r0, KParams kp) {
@@ -374,11 +360,11 @@ __global__ void __launch_bounds__(SYM_THREADS, H2B_SYM_MINB)
   }
 }
 
-template <int D, int KIND, bool F32S>
-void launch_sym(const DevH2& h, int64_t R, int64_t r0, const KParams& kp, cudaStream_t s) {
+template <int D, int KIND, int TB, int MINB, bool F32S>
+void launch_sym_width(const DevH2& h, int64_t R, int64_t r0, const KParams& kp, cudaStream_t s) {
   if (!h.n_sym_items) return;
   const int L = h.t->depth;
-  auto kern = interact_sym<D, KIND, H2B_SYM_RS, H2B_SYM_TB, F32S>;
+  auto kern = interact_sym<D, KIND, H2B_SYM_RS, TB, MINB, F32S>;
   int dev = 0, nsm = 0, per = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -388,6 +374,16 @@ void launch_sym(const DevH2& h, int64_t R, int64_t r0, const KParams& kp, cudaSt
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, SYM_THREADS, smem));
   const int64_t grid = std::min<int64_t>((int64_t)nsm * std::max(per, 1),
                                          (h.n_sym_items + SYM_THREADS / 32 - 1) / (SYM_THREADS / 32));
+  CK(cudaMemsetAsync(h.work_counter.get(), 0, sizeof(unsigned long long), s));
+  kern<<<(unsigned)grid, SYM_THREADS, smem, s>>>(h.sym_items.get(), reinterpret_cast<const int4*>(h.sym_desc.get()),
+                                                 h.n_sym_items, h.work_counter.get(),
+                                                 reinterpret_cast<const SymTab*>(h.sym_tabs.get()), ntabs, L + 1,
+                                                 R, r0, kp);
+  CKL();
+}
+
+template <int D, int KIND, bool F32S>
+void launch_sym(const DevH2& h, int64_t R, int64_t r0, const KParams& kp, cudaStream_t s) {
   // one RHS of a wider product: pack this column's charges into the records (the gather / upward pass wrote
   // them already when R == 1)
   const auto& pk = h.pack1;
@@ -396,12 +392,13 @@ void launch_sym(const DevH2& h, int64_t R, int64_t r0, const KParams& kp, cudaSt
                                                            pk.nlists, pk.total, R, r0, 0);
     CKL();
   }
-  CK(cudaMemsetAsync(h.work_counter.get(), 0, sizeof(unsigned long long), s));
-  kern<<<(unsigned)grid, SYM_THREADS, smem, s>>>(h.sym_items.get(), reinterpret_cast<const int4*>(h.sym_desc.get()),
-                                              h.n_sym_items, h.work_counter.get(),
-                                              reinterpret_cast<const SymTab*>(h.sym_tabs.get()), ntabs, L + 1,
-                                              R, r0, kp);
-  CKL();
+#ifndef H2B_SYM_FORCE
+#define H2B_SYM_FORCE 0  // tuning builds: 16 or 32 forces the chunk width
+#endif
+  if (H2B_SYM_FORCE == 32 || (H2B_SYM_FORCE == 0 && h.sym_wide))
+    launch_sym_width<D, KIND, 32, 3, F32S>(h, R, r0, kp, s);
+  else
+    launch_sym_width<D, KIND, 16, 4, F32S>(h, R, r0, kp, s);
 }
 
 template <int D, int KIND>

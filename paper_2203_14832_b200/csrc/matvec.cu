@@ -387,7 +387,8 @@ __global__ void item_costs(int64_t n, int lev, const int64_t* __restrict__ t_ptr
 // leaf's own block)
 __global__ void sym_costs(int64_t n, int lst, int near, const int64_t* __restrict__ ptr,
                           const int64_t* __restrict__ l_ptr, const int64_t* __restrict__ l_idx,
-                          unsigned long long* __restrict__ cost, int64_t* __restrict__ item) {
+                          unsigned long long* __restrict__ cost, int64_t* __restrict__ item,
+                          unsigned long long* __restrict__ class_pairs) {
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= n) return;
   const int64_t m = ptr[c + 1] - ptr[c];
@@ -400,6 +401,11 @@ __global__ void sym_costs(int64_t n, int lst, int near, const int64_t* __restric
   // time: both together overflow the instruction cache), each by pair count
   const unsigned long long band = near ? 1ull : 2ull;
   cost[c] = (m > 0 && src > 0) ? (band << 56) | ((unsigned long long)(m * src) + 1ull) : 0ull;
+  if (m > 0 && src > 0) {  // source passes (64 records) x target chunks of 16 / of 32
+    const unsigned long long passes = (unsigned long long)((src + 63) / 64);
+    atomicAdd(class_pairs, passes * (unsigned long long)((m + 15) / 16));
+    atomicAdd(class_pairs + 1, passes * (unsigned long long)((m + 31) / 32));
+  }
   item[c] = ((int64_t)lst << 40) | c;
 }
 
@@ -509,14 +515,16 @@ void build_sym(DevH2& h, cudaStream_t s) {
     sb[l].l_ptr = nf ? Lv.nb_ptr.get() : Lv.il_ptr.get();
     sb[l].u_cnt = h.u_cnt[l].get();
   }
-  // items
+  // items, and the pair counts of narrow (<= 16 targets) and wide items
   int64_t total = T.lv[L].n;
   for (int l = 2; l <= L; l++) total += T.lv[l].n;
-  DBuf<unsigned long long> cost, cost_sorted;
+  DBuf<unsigned long long> cost, cost_sorted, class_pairs;
   DBuf<int64_t> item;
   cost.alloc(std::max<int64_t>(total, 1));
   cost_sorted.alloc(std::max<int64_t>(total, 1));
   item.alloc(std::max<int64_t>(total, 1));
+  class_pairs.alloc(2);
+  CK(cudaMemsetAsync(class_pairs.get(), 0, 2 * sizeof(unsigned long long), s));
   h.sym_items.alloc(std::max<int64_t>(total, 1), &h.mem);
   int64_t off = 0;
   for (int l : ids) {
@@ -525,7 +533,7 @@ void build_sym(DevH2& h, cudaStream_t s) {
     if (Lv.n)
       sym_costs<<<nblk(Lv.n, 256), 256, 0, s>>>(Lv.n, l, nf ? 1 : 0, sb[l].ptr, sb[l].l_ptr,
                                                 nf ? Lv.nb_idx.get() : Lv.il_idx.get(), cost.get() + off,
-                                                item.get() + off);
+                                                item.get() + off, class_pairs.get());
     CKL();
     off += Lv.n;
   }
@@ -537,8 +545,17 @@ void build_sym(DevH2& h, cudaStream_t s) {
   CK(cub::DeviceRadixSort::SortPairsDescending(tmp.get(), bytes, cost.get(), cost_sorted.get(), item.get(),
                                                h.sym_items.get(), total, 0, 64, s));
   auto hc = to_host(cost_sorted.get(), total, s);
+  auto cp = to_host(class_pairs.get(), 2, s);
   int64_t nz = 0;
   while (nz < total && hc[nz] > 0) nz++;
+  // one chunk width for the whole product (measured: splitting the items over two launches costs more in tail
+  // effects than the better width per item saves).  32-target chunks run 12 instead of 16 warps per SM; they
+  // pay off when they cut the (chunk, source pass) steps by > 30% AND items are long (many passes per chunk:
+  // c1 ~140 steps per item, 6.37 vs 7.38 ms), not for the headline's short items (c2 ~13: 1.63 vs 1.61 ms)
+  h.sym_wide = (double)cp[1] < 0.7 * (double)cp[0] && (double)cp[0] > 40.0 * (double)std::max<int64_t>(nz, 1);
+  if (getenv("H2B_SETUP_VERBOSE"))
+    fprintf(stderr, "[h2b] symmetric kernel: %lld items, %llu (chunk, pass) steps with 16-target chunks, %llu with 32\n",
+            (long long)nz, cp[0], cp[1]);
   h.n_sym_items = nz;
   DBuf<SymBuild> dsb;
   dsb.alloc(sb.size());
@@ -786,12 +803,17 @@ int64_t matvec_launches(const DevH2& h, int64_t nrhs) {
   const int L = h.t->depth;
   std::vector<std::pair<int64_t, int>> ch;
   rhs_chunks(nrhs, ch);
-  int64_t nchunk = (int64_t)ch.size();
-  // gather, P2M, M2M x (L-2), (record pack + interaction) x chunks, L2L x (L-2), L2P+scatter;
-  // one RHS: the gather and the upward pass write the records (no pack launch)
-  const int64_t per_chunk = nrhs == 1 ? 1 : 2;
-  if (L < 2) return 1 + per_chunk * nchunk + 1;
-  return 1 + 1 + (L - 2) + per_chunk * nchunk + (L - 2) + 1;
+  // gather, P2M, M2M x (L-2), interaction launches per RHS chunk, L2L x (L-2), L2P+scatter.  Per chunk: a record
+  // pack unless one RHS (the gather and the upward pass write the records), then the interaction kernel (one
+  // launch)
+  const bool sym = h.symmetric && h.sym_ready && (nrhs % 16) != 0;
+  int64_t inter = 0;
+  for (auto& c : ch) {
+    inter += nrhs == 1 ? 0 : 1;
+    inter += (sym && c.second == 1) ? (h.n_sym_items > 0) : 1;
+  }
+  if (L < 2) return 1 + inter + 1;
+  return 1 + 1 + (L - 2) + inter + (L - 2) + 1;
 }
 
 void matvec(DevH2& h, const double* w, double* u, int64_t R, cudaStream_t s) {

@@ -45,17 +45,30 @@ CONFIGS = {
     "c4": ("uniform", 4194304, 2, 4, "coulomb-3d", {}, 128, 1e-10, "normal", 16),
 }
 HEADLINE = "c2"
-# FP64 flops the interaction kernel executes per 1/r pair (DFMA = 2, DADD / DMUL = 1; MUFU.RSQ64H seed not
-# counted), one RHS; each further RHS adds one DFMA (2 flops):
-#   M2L (interact.cuh pair_r2 + acc_inv_r): r^2 = DADD + 3 DFMA (7); from the FP32-MUFU seed
-#        (rsq_seed_f32, integer exponent rebase) one quadratic step DMUL + DFMA (3); charge DMUL +
-#        accumulate DFMA (3)                                                                      -> 13
-#        (H2B_F32SEED=0 or a geometry outside the FP32 range: MUFU.RSQ64H seed + cubic step
-#        DMUL + 3 DFMA (7)                                                                         -> 17)
-#   near field: r^2 = 3 DADD + 3 DFMA (9); quadratic step DMUL + DFMA (3); DMUL + DFMA (3)       -> 15
-# The bench configs all lie in [-1, 1]^d, inside the FP32-seed guard (interact.cuh f32seed_ok).
-FLOPS_PER_PAIR_M2L = 13 if os.environ.get("H2B_F32SEED", "1") != "0" else 17
-FLOPS_PER_PAIR_NEAR = 15
+
+# ---- roofline models ----
+# Nominal FP64 peak of a B200: 148 SMs x 64 DFMA/clk x 2 flop x the max SM clock (1965 MHz) = 37.2 TFLOP/s.
+# MEASURED_PEAKS.json has no FP64 entry; the in-run DFMA probe (h2b_fp64_peak, ~34 TFLOP/s) is printed beside it.
+NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+HBM_PEAK_GBS_FALLBACK = 6450.6  # MEASURED_PEAKS.json hbm_gbs when present (read at run time)
+# Executed FP64 flops per evaluated pair (DFMA = 2, DADD / DMUL = 1; the MUFU seeds and the integer exponent
+# rebase are not counted), one RHS:
+#   symmetric kernel (interact_sym.cuh), each unordered pair evaluated once and applied both ways:
+#     M2L  r^2 = DADD + 3 DFMA (7); K = DMUL + DFMA + DMUL (4, FP32 seed + one quadratic step);
+#          row and column accumulations 2 DFMA (4)                                                   -> 15
+#     near r^2 = 3 DADD + 3 DFMA (9); K 4; accumulations 4                                          -> 17
+#          (the leaf's own block is evaluated in both orders; the other near pairs once)
+#   one-directional kernel (interact.cuh; multi-RHS chunks): M2L 13 + 2 per further RHS, near 15 + 2 per RHS
+SYM_FLOPS_M2L, SYM_FLOPS_NEAR = 15, 17
+DIR_FLOPS_M2L, DIR_FLOPS_NEAR = 13, 15
+
+
+def hbm_peak_gbs():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        return float(json.load(open(path))["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, ValueError, KeyError):
+        return HBM_PEAK_GBS_FALLBACK, "fallback (last measured copy bandwidth on this pool)"
 
 
 def make_inputs(cfg, n_override=None):
@@ -206,7 +219,7 @@ def run_reference(args, cfg, world, rank):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "N^2/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name(args, cfg, n), "N": n},
+        "config": config_dict(args, cfg, n),
         "matvec_ms": ms, "setup_ms": 1e3 * res["setup_s"],
         "cpu_baseline": {"value": value, "unit": "N^2/s", "cores": res["threads"], "kind": "port",
                          "sample": f"full workload: oracle setup once + {args.warmup}+{args.steps} full matvecs at "
@@ -214,6 +227,12 @@ def run_reference(args, cfg, world, rank):
         "e2e": {"value": value, "unit": "N^2/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def config_dict(args, cfg, n):
+    """The workload identity, identical in both arms (the driver compares them)."""
+    nrhs = cfg[9]
+    return {"workload": workload_name(args, cfg, n), "N": n, "nrhs": nrhs}
 
 
 def workload_name(args, cfg, n):
@@ -290,31 +309,94 @@ def run_b200(args, cfg, world, rank, local):
     ms = max_over_ranks(float(np.mean(per)), world)
     value = aggregate_value(n, ms, world)
 
-    # ---- e2e: through the C ABI with pinned host buffers (H2D + matvec + D2H per step) ----
+    # ---- e2e: the public drop-in call h2_matvec(h2, w) on pinned host tensors (H2D + matvec + D2H per step,
+    # inside the timed region; the call returns after the result is on the host) ----
     wh = torch.from_numpy(np.ascontiguousarray(w)).pin_memory()
     uh = torch.empty(tuple(ud.shape), dtype=torch.float64).pin_memory()
     for _ in range(2):
-        _lib.check(L.h2b_matvec(h2.handle, wh.data_ptr(), uh.data_ptr(), nrhs, 0, stream.cuda_stream))
+        h2c.h2_matvec(h2, wh, out=uh)
     ee = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     barrier(world)
     for e0, e1 in ee:
         flush.zero_()
         e0.record(stream)
-        _lib.check(L.h2b_matvec(h2.handle, wh.data_ptr(), uh.data_ptr(), nrhs, 0, stream.cuda_stream))
+        h2c.h2_matvec(h2, wh, out=uh)
         e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(float(np.mean([e0.elapsed_time(e1) for e0, e1 in ee])), world)
     e2e_value = aggregate_value(n, e2e_ms, world)
+    # the same call on plain (pageable) numpy arrays, host wall clock (reported beside, not the headline)
+    wn, un = np.ascontiguousarray(w), np.empty(tuple(ud.shape))
+    h2c.h2_matvec(h2, wn, out=un)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        h2c.h2_matvec(h2, wn, out=un)
+    e2e_numpy_ms = 1e3 * (time.perf_counter() - t0) / args.steps
 
-    # ---- roofline of the dominant kernel family (FP64 interaction kernel: M2L + near field) ----
+    # ---- roofline of the dominant kernel (FP64 interaction: M2L + near field), the transfer passes and setup ----
     st = h2.native_stats()
     pairs_m2l, pairs_p2p = int(st[1]), int(st[2])
-    stage = stage_times(h2, wd, repeats=max(3, min(args.steps, 10)))  # [up, m2l, l2l, near+l2p, total]
-    peak = ctypes_peak(L)
-    inter_ms = stage[1] + stage[3]
-    flops = pairs_m2l * (FLOPS_PER_PAIR_M2L + 2 * (nrhs - 1)) + pairs_p2p * (FLOPS_PER_PAIR_NEAR + 2 * (nrhs - 1))
+    depth = int(st[8])
+    stage = stage_times(h2, wd, repeats=max(3, min(args.steps, 10)))  # [up, m2l+near, l2l, l2p, total]
+    probe = ctypes_peak(L)
+    sym = bool(st[6]) and nrhs % 16 != 0
+    leaf_sizes = np.diff(tree.array(depth, "t_ptr")) if depth >= 0 else np.zeros(0)
+    self_pairs = int(np.sum(leaf_sizes.astype(np.int64) ** 2))
+    if sym:
+        evaluated = {"m2l": pairs_m2l // 2, "near": (pairs_p2p - self_pairs) // 2 + self_pairs}
+        flops = evaluated["m2l"] * SYM_FLOPS_M2L + evaluated["near"] * SYM_FLOPS_NEAR
+        fpp = {"m2l": SYM_FLOPS_M2L, "near": SYM_FLOPS_NEAR, "per": "evaluated unordered pair"}
+    else:
+        evaluated = {"m2l": pairs_m2l, "near": pairs_p2p}
+        flops = pairs_m2l * (DIR_FLOPS_M2L + 2 * (nrhs - 1)) + pairs_p2p * (DIR_FLOPS_NEAR + 2 * (nrhs - 1))
+        fpp = {"m2l": DIR_FLOPS_M2L + 2 * (nrhs - 1), "near": DIR_FLOPS_NEAR + 2 * (nrhs - 1),
+               "per": "applied entry (one-directional kernel)"}
+    inter_ms = stage[1]
     achieved = flops / (inter_ms * 1e-3) / 1e12
-    traffic = load_traffic()
+    traffic, traffic_src = load_traffic(args.config)
+    hbm_peak, hbm_src = hbm_peak_gbs()
+    # transfer passes: algorithmic bytes = the interpolation operators read once per product (P2M / M2M read
+    # the column interpolators, L2L / L2P the row interpolators; pmat per level = sum over cells of rows x k) plus
+    # the coefficient vectors they stream (w in, pivot coefficients written and read, u out), nrhs columns each
+    op_bytes = 0
+    vec_bytes = 8 * nrhs * (2 * n)  # w_sorted read + u written (near-field partials read by L2P: + n)
+    vec_bytes += 8 * nrhs * n
+    for lev in range(2, depth + 1):
+        m_in, k_in = h2.array(lev, "m_in"), h2.array(lev, "k_in")
+        n_out, k_out = h2.array(lev, "n_out"), h2.array(lev, "k_out")
+        op_bytes += 8 * int(np.dot(m_in, k_in)) + 8 * int(np.dot(n_out, k_out))
+        vec_bytes += 8 * nrhs * 4 * int(k_in.sum())  # coefficients: written + read up, read + written down
+    tr_ms = stage[0] + stage[2] + stage[3]
+    tr_bytes = op_bytes + vec_bytes
+    # setup: the ACA's residual sweeps (reference operation order, _core.pyx:70-191): step t re-reads the t previous
+    # residual rows / columns of the cell's block (n + m entries each), once for the residual and once for the
+    # stopping test's cross products.  nevals per cell ~ k (n + m), so operand bytes ~ 8 (k - 1) nevals and
+    # FP64 flops ~ 4 (k - 1) / 2 * 2 nevals (one FMA per operand entry and sweep)
+    aca_bytes = aca_flops = 0
+    for lev in range(2, depth + 1):
+        k_in, nev = h2.array(lev, "k_in").astype(np.float64), h2.array(lev, "nevals").astype(np.float64)
+        aca_bytes += 8.0 * float(np.dot(np.maximum(k_in - 1, 0), nev))
+        aca_flops += 2.0 * float(np.dot(np.maximum(k_in - 1, 0), nev))
+    setup_s = (tree_ms + nnca_ms) * 1e-3
+    roof_inter = {"bound": "fp64", "kernel": "interact_sym (M2L all levels + near field)" if sym else
+                  "interact_warps (M2L all levels + near field)",
+                  "achieved": achieved, "peak": NOMINAL_FP64_TFLOPS, "unit": "TFLOP/s",
+                  "frac": achieved / NOMINAL_FP64_TFLOPS, "traffic": traffic, "traffic_source": traffic_src,
+                  "peak_source": "nominal B200 FP64 (148 SM x 64 DFMA/clk x 2 x 1965 MHz); MEASURED_PEAKS.json "
+                                 "has no FP64 entry",
+                  "fp64_probe_tflops": probe, "frac_of_probe": achieved / probe,
+                  "flops": flops, "ms": inter_ms, "flops_per_pair": fpp, "evaluated_pairs": evaluated,
+                  "applied_entries_per_s": (pairs_m2l + pairs_p2p) / (inter_ms * 1e-3)}
+    roof_tr = {"bound": "hbm", "kernel": "up_rows/down_rows/l2p_rows (P2M, M2M, L2L, L2P)",
+               "achieved": tr_bytes / (tr_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+               "frac": tr_bytes / (tr_ms * 1e-3) / 1e9 / hbm_peak, "bytes": tr_bytes, "operator_bytes": op_bytes,
+               "ms": tr_ms, "peak_source": hbm_src}
+    roof_setup = {"n2_per_s": float(n) ** 2 / setup_s, "ms": setup_s * 1e3,
+                  "aca_operand_bytes_model": aca_bytes, "aca_achieved_GBps": aca_bytes / (nnca_ms * 1e-3) / 1e9,
+                  "aca_frac_hbm": aca_bytes / (nnca_ms * 1e-3) / 1e9 / hbm_peak,
+                  "aca_flops_model": aca_flops, "aca_achieved_tflops": aca_flops / (nnca_ms * 1e-3) / 1e12,
+                  "aca_frac_fp64": aca_flops / (nnca_ms * 1e-3) / 1e12 / NOMINAL_FP64_TFLOPS,
+                  "note": "model: the residual sweeps mostly hit L2, so the HBM fraction can read > 1"}
 
     # ---- accuracy: sampled dense rows + CPU-oracle H2 matvec at the full N ----
     uhost = ud.cpu().numpy()
@@ -329,22 +411,21 @@ def run_b200(args, cfg, world, rank, local):
         "metric": METRIC, "value": value, "unit": "N^2/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; stands in for the paper's point sets)",
-        "config": {"workload": workload_name(args, cfg, n), "N": n, "nrhs": nrhs,
-                   "l2": "flushed (256 MB write) between timed steps", "parallelism": f"replicas x{world}"},
+        "config": config_dict(args, cfg, n),
+        "l2": "flushed (256 MB write) between timed steps", "parallelism": f"replicas x{world}",
         "matvec_ms": ms, "setup_ms": tree_ms + nnca_ms, "tree_ms": tree_ms, "nnca_ms": nnca_ms,
-        "setup_first_ms": sum(setups[0]),
-        "depth": int(st[8]), "max_rank": int(st[3]), "m2l_pairs": pairs_m2l, "p2p_pairs": pairs_p2p,
-        "stage_ms": {"upward": stage[0], "m2l": stage[1], "l2l": stage[2], "near_l2p": stage[3], "total": stage[4]},
-        "rel_l2_err_dense_1000_rows": err_dense,
+        "setup_first_ms": sum(setups[0]), "setup_n2_per_s": float(n) ** 2 / setup_s,
+        "depth": depth, "max_rank": int(st[3]), "m2l_pairs": pairs_m2l, "p2p_pairs": pairs_p2p,
+        "stage_ms": {"upward": stage[0], "interaction": stage[1], "l2l": stage[2], "l2p": stage[3],
+                     "total": stage[4]},
+        "rel_l2_err_dense_1000_rows": err_dense, "eps": cfg[7], "eps_ratio": err_dense / cfg[7],
         "e2e": {"value": e2e_value, "unit": "N^2/s", "ms_per_step": e2e_ms, "h2d_bytes_per_step": int(wh.nbytes),
-                "d2h_bytes_per_step": int(uh.nbytes)},
+                "d2h_bytes_per_step": int(uh.nbytes),
+                "call": "paper_2203_14832_b200.h2_matvec(h2, w_pinned, out=u_pinned) (C ABI h2b_matvec, host "
+                        "pointers)"},
+        "e2e_numpy_ms": e2e_numpy_ms,
         "gpu_launches": int(matvec_launches(h2, nrhs)) * args.steps,
-        "roofline": {"bound": "fp64", "kernel": "interact_kernel (M2L all levels + near field/L2P)",
-                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                     "traffic": traffic,
-                     "flops_per_pair": {"m2l": FLOPS_PER_PAIR_M2L, "near": FLOPS_PER_PAIR_NEAR},
-                     "pairs_per_s": (pairs_m2l + pairs_p2p) / (inter_ms * 1e-3),  # kernel evaluations (each serves nrhs columns)
-                     "peak_source": "measured: DFMA throughput probe (h2b_fp64_peak) on this GPU, same run"},
+        "roofline": dict(roof_inter, transfers=roof_tr, setup=roof_setup),
         "clocks": clk.summary(),
     }
     if rank == 0 and not args.no_cpu_baseline and args.gpus == 1 and world == 1:
@@ -368,15 +449,18 @@ def ctypes_peak(L):
     return v.value
 
 
-def load_traffic():
-    """dram bytes per launch of the interaction kernel from the committed ncu summary, if any."""
+def load_traffic(config):
+    """DRAM bytes per launch of the interaction kernel (dram__bytes_read.sum + dram__bytes_write.sum) from the
+    committed ncu --set full capture of the current kernel, if any (profiles/interact_traffic.json)."""
     path = os.path.join(REPO, "profiles", "interact_traffic.json")
-    if os.path.exists(path):
-        try:
-            return json.load(open(path)).get("dram_bytes_per_launch")
-        except (OSError, ValueError):
-            return None
-    return None
+    try:
+        d = json.load(open(path))
+        e = d.get(config)
+        if e:
+            return e["dram_bytes_per_launch"], e["source"]
+    except (OSError, ValueError, KeyError):
+        pass
+    return None, "no ncu capture of this kernel at this config committed"
 
 
 def main():

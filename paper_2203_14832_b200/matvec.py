@@ -1,11 +1,12 @@
 """H2 matrix-vector product, dense oracle and error metrics (matvec.py of h2cross).
 
 ``h2_matvec`` runs the level-batched GPU product (h2b_matvec): P2M, M2M,
-M2L at every level with the coupling entries regenerated in registers, L2L,
-and one fused near-field + L2P kernel that writes the result in the caller's
-point order.  Accepts numpy arrays (host in / host out, copies included) or
-float64 CUDA torch tensors (device-resident, zero copy, runs on the current
-torch stream).  ``w`` may be (n,) as in the reference or (n, nrhs).
+M2L at every level and the near field with the coupling entries regenerated
+in registers (on the symmetric path each unordered cell pair once, applied
+both ways), L2L, and L2P, writing the result in the caller's point order.
+Accepts numpy arrays, CPU torch tensors (pinned: asynchronous copies) or
+float64 CUDA torch tensors (device-resident, zero copy, current torch
+stream).  ``w`` may be (n,) as in the reference or (n, nrhs).
 """
 
 from __future__ import annotations
@@ -17,47 +18,67 @@ from .compress import H2Matrix
 from .kernels import KernelSpec
 
 
-def _is_torch_cuda(x) -> bool:
-    mod = type(x).__module__
-    return mod.startswith("torch") and getattr(x, "is_cuda", False)
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
 
 
-def h2_matvec(h2: H2Matrix, w):
-    """Apply the compressed operator: u = A w (matvec.py:483)."""
+def h2_matvec(h2: H2Matrix, w, out=None):
+    """Apply the compressed operator: u = A w (matvec.py:142).
+
+    ``w`` is (n,) as in the reference or (n, nrhs); float64.  Accepted forms:
+
+    * numpy array: host in / host out (the copies go through the driver's staging);
+    * CPU torch tensor, ideally pinned (``pin_memory()``): host in / host out with asynchronous copies on the
+      current CUDA stream -- the end-to-end path ``bench.py`` times;
+    * CUDA torch tensor: device-resident, zero copy, on the current torch stream.
+
+    ``out`` (same kind and shape as the result) avoids allocating the result on every call.
+    """
     n_t, n_s = h2.shape
     L = _lib.lib()
-    if _is_torch_cuda(w):
+    if _is_torch(w):
         import torch
 
         if w.dtype != torch.float64:
-            raise ValueError("device vectors must be float64")
-        if w.shape[0] != n_s or w.dim() not in (1, 2):
+            raise ValueError("vectors must be float64")
+        if w.dim() not in (1, 2) or w.shape[0] != n_s:
             raise ValueError(f"vector has shape {tuple(w.shape)}, expected ({n_s},) or ({n_s}, nrhs)")
         w = w.contiguous()
         nrhs = 1 if w.dim() == 1 else w.shape[1]
-        u = torch.empty((n_t,) if w.dim() == 1 else (n_t, nrhs), dtype=torch.float64, device=w.device)
-        stream = torch.cuda.current_stream(w.device).cuda_stream
-        _lib.check(L.h2b_matvec(h2.handle, w.data_ptr(), u.data_ptr(), nrhs, 1, stream))
-        return u
+        shape = (n_t,) if w.dim() == 1 else (n_t, nrhs)
+        if out is None:
+            out = torch.empty(shape, dtype=torch.float64, device=w.device, pin_memory=bool(not w.is_cuda
+                                                                                            and w.is_pinned()))
+        elif tuple(out.shape) != shape or out.dtype != torch.float64 or out.device != w.device or \
+                not out.is_contiguous():
+            raise ValueError(f"out must be a contiguous float64 tensor of shape {shape} on {w.device}")
+        dev = w.device if w.is_cuda else torch.device("cuda", torch.cuda.current_device())
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        _lib.check(L.h2b_matvec(h2.handle, w.data_ptr(), out.data_ptr(), nrhs, 1 if w.is_cuda else 0, stream))
+        return out
     w = np.asarray(w, dtype=np.float64)
     if w.ndim not in (1, 2) or w.shape[0] != n_s:
         raise ValueError(f"vector has shape {w.shape}, expected ({n_s},)")
     w = np.ascontiguousarray(w)
     nrhs = 1 if w.ndim == 1 else w.shape[1]
-    u = np.empty((n_t,) if w.ndim == 1 else (n_t, nrhs))
-    _lib.check(L.h2b_matvec(h2.handle, w.ctypes.data, u.ctypes.data, nrhs, 0, None))
-    return u
+    shape = (n_t,) if w.ndim == 1 else (n_t, nrhs)
+    if out is None:
+        out = np.empty(shape)
+    elif out.shape != shape or out.dtype != np.float64 or not out.flags.c_contiguous:
+        raise ValueError(f"out must be a C-contiguous float64 array of shape {shape}")
+    _lib.check(L.h2b_matvec(h2.handle, w.ctypes.data, out.ctypes.data, nrhs, 0, None))
+    return out
 
 
 def h2_matvec_reference(h2: H2Matrix, w, collect: bool = False):
-    """matvec.py:510 — the engine has a single (device) product; ``collect`` is unsupported."""
+    """matvec.py:169 — the engine has a single (device) product; ``collect`` is unsupported."""
     if collect:
         raise NotImplementedError("per-cell coefficient collection is not exposed by the B200 engine")
     return h2_matvec(h2, w)
 
 
 def dense_matvec(kernel: KernelSpec, cloud, w):
-    """Exact O(N^2) product by direct evaluation on the GPU (matvec.py:574)."""
+    """Exact O(N^2) product by direct evaluation on the GPU (matvec.py:233)."""
     kernel.require_device()
     w = np.asarray(w, dtype=np.float64)
     if w.shape[0] != cloud.n_sources or w.ndim not in (1, 2):
@@ -73,7 +94,7 @@ def dense_matvec(kernel: KernelSpec, cloud, w):
 
 
 def dense_rows(kernel: KernelSpec, cloud, rows, w) -> np.ndarray:
-    """Exact values of selected output rows (matvec.py:586), on the GPU."""
+    """Exact values of selected output rows (matvec.py:245), on the GPU."""
     kernel.require_device()
     rows = _lib.i64(rows)
     w = _lib.f64(w)
@@ -85,7 +106,7 @@ def dense_rows(kernel: KernelSpec, cloud, rows, w) -> np.ndarray:
 
 
 def relative_error(u, u_ref) -> float:
-    """||u - u_ref||_2 / ||u_ref||_2 (matvec.py:592)."""
+    """||u - u_ref||_2 / ||u_ref||_2 (matvec.py:251)."""
     u = np.asarray(u, dtype=np.float64)
     u_ref = np.asarray(u_ref, dtype=np.float64)
     if u.shape != u_ref.shape:

@@ -18,7 +18,7 @@ def pytest_configure(config):
 
 def golden_names():
     return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
-                  if not p.endswith(("aca_blocks.npz", "extras.npz")))
+                  if not p.endswith("aca_blocks.npz"))
 
 
 def load_golden(name):

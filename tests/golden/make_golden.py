@@ -239,29 +239,5 @@ def main():
         print("wrote aca_blocks")
 
 
-if __name__ == "__main__" and "--extras" not in sys.argv:
+if __name__ == "__main__":
     main()
-
-
-def extras(h):
-    """Reference outputs for the rows next to the path (SVM dataset generator, Fredholm solve)."""
-    from h2cross.krylov import solve_fredholm
-    from h2cross.svm import synth_dataset
-
-    out = {}
-    for shape, m, seed in (("rings2d", 300, 0), ("hypersphere4d", 257, 5)):
-        ds = synth_dataset(shape, m, seed=seed)
-        out[f"{shape}_features"] = ds.features
-        out[f"{shape}_labels"] = ds.labels
-        out[f"{shape}_train"] = ds.train_mask
-    rep, err, _ = solve_fredholm(8, epsilon_nca=1e-7, epsilon_gmres=1e-10, seed=0)
-    out["fredholm8_iter"] = np.int64(rep.iterations)
-    out["fredholm8_err"] = np.float64(err)
-    out["fredholm8_history"] = np.array(rep.residual_history)
-    out["fredholm8_solution"] = rep.solution
-    np.savez_compressed(os.path.join(HERE, "extras.npz"), **out)
-    print("wrote extras")
-
-
-if __name__ == "__main__" and "--extras" in sys.argv:
-    extras(build_reference("/root/reference/pkg"))

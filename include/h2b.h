@@ -37,19 +37,19 @@ enum {
 const char* h2b_last_error(void);
 int h2b_version(void);
 
-/* ---- fused kernel evaluation: _accel/_core.pyx:161 kernel_block ---- */
+/* ---- fused kernel evaluation: _accel/_core.pyx:47 kernel_block ---- */
 int h2b_kernel_block(int kind, double a, const double* X, int64_t m, const double* Y, int64_t n, int d,
                      double* out);
-/* _accel/_core.pyx:173 kernel_row */
+/* _accel/_core.pyx:59 kernel_row */
 int h2b_kernel_row(int kind, double a, const double* x, const double* Y, int64_t n, int d, double* out);
-/* _accel/_core.pyx:184 aca_kernel: partially pivoted ACA on K(X_i, Y_j).
+/* _accel/_core.pyx:70 aca_kernel: partially pivoted ACA on K(X_i, Y_j).
  * U (m x cap) and V (n x cap) row-major, first *rank columns valid;
  * rp / cp: local pivots in discovery order. */
 int h2b_aca_kernel(int kind, double a, const double* X, int64_t m, const double* Y, int64_t n, int d,
                    double eps, int64_t cap, double* U, double* V, int64_t* rp, int64_t* cp, int* converged,
                    int64_t* nevals, int64_t* rank);
 
-/* ---- tree: geometry.py:293 build_tree (+ :402 compute_lists) ---- */
+/* ---- tree: geometry.py:230 build_tree (+ :339 compute_lists) ---- */
 int h2b_tree_build(const double* P, int64_t np, const double* Q, int64_t nq, int d, int shared, int64_t nu,
                    double eta, int on_device, void* stream, h2b_tree** out);
 void h2b_tree_free(h2b_tree* t);
@@ -58,7 +58,7 @@ int h2b_tree_info(const h2b_tree* t, int* depth, int* over_capacity, double* mid
 /* number of nonempty cells at a level */
 int64_t h2b_tree_ncells(const h2b_tree* t, int level);
 /* Per-level arrays in the reference's cell order (nonempty cells sorted by
- * multi-index, geometry.py:238).  what: 0 key 1 multi_index(n*d) 2 t_ptr
+ * multi-index, geometry.py:175).  what: 0 key 1 multi_index(n*d) 2 t_ptr
  * 3 t_idx 4 s_ptr 5 s_idx 6 nb_ptr 7 nb_idx 8 il_ptr 9 il_idx 10 parent
  * 11 ch_ptr 12 ch_idx.  Returns the element count; copies when dst != 0. */
 int64_t h2b_tree_get(const h2b_tree* t, int level, int what, int64_t* dst);
@@ -80,7 +80,7 @@ int64_t h2b_h2_get_interp(const h2b_h2* h, int level, int64_t cell, int which, i
  * cells_visited memory_bytes symmetric setup_ns depth aca_unconverged */
 int h2b_h2_stats(const h2b_h2* h, int64_t* stats);
 
-/* ---- matvec: matvec.py:483 h2_matvec ---- */
+/* ---- matvec: matvec.py:142 h2_matvec ---- */
 /* w: (n_sources, nrhs) row-major, u: (n_targets, nrhs). */
 int h2b_matvec(const h2b_h2* h, const double* w, double* u, int64_t nrhs, int on_device, void* stream);
 /* Number of kernel launches one h2b_matvec call issues (for bench accounting). */
@@ -93,7 +93,7 @@ int h2b_last_stage_ms(double* ms5);
  * denominator for the FP64-bound interaction kernels. */
 int h2b_fp64_peak(double* tflops);
 
-/* ---- dense oracles: matvec.py:574 dense_matvec / :586 dense_rows ---- */
+/* ---- dense oracles: matvec.py:233 dense_matvec / :245 dense_rows ---- */
 int h2b_dense_matvec(int kind, double a, const double* P, int64_t np, const double* Q, int64_t nq, int d,
                      const double* w, double* u, int64_t nrhs, int on_device, void* stream);
 int h2b_dense_rows(int kind, double a, const double* P, const int64_t* rows, int64_t nrows, const double* Q,

@@ -9,7 +9,7 @@
  * Floating-point contract: compiled with -ffp-contract=off so every
  * expression rounds exactly as the reference's Cython core (_core.pyx,
  * built with plain -O3, no FMA) does.  The one place the reference goes
- * through OpenBLAS (np.dot in geometry.py:215) is restated with explicit
+ * through OpenBLAS (np.dot in geometry.py:152) is restated with explicit
  * fma() in sequence, which is what that ddot kernel computes for d <= 8
  * (checked against numpy in tests/test_oracle_golden.py).
  */
@@ -25,7 +25,7 @@
 #endif
 
 #define MAXD 8
-#define WIDTH_UNDERFLOW 0x1p-50 /* geometry.py:99 */
+#define WIDTH_UNDERFLOW 0x1p-50 /* geometry.py:36 */
 #define TOP_COMPRESSED_LEVEL 2  /* compress.py:40 */
 static const double INV_FOUR_PI = 0.07957747154594767; /* 1/(4 pi), correctly rounded */
 
@@ -67,7 +67,7 @@ static void* xcalloc(size_t n, size_t s) {
 }
 
 /* ------------------------------------------------------------------ */
-/* kernels: _core.pyx:129 _kval, :152 _r2                              */
+/* kernels: _core.pyx:15 _kval, :38 _r2                              */
 /* ------------------------------------------------------------------ */
 double oh2_kval(int kind, double a, double r2) {
   double r;
@@ -108,7 +108,7 @@ void oh2_kernel_block(int kind, double a, const double* X, int64_t m, const doub
 }
 
 /* ------------------------------------------------------------------ */
-/* geometry: geometry.py:210 boxes_admissible                          */
+/* geometry: geometry.py:147 boxes_admissible                          */
 /* ------------------------------------------------------------------ */
 int oh2_boxes_admissible(const double* cx, double hwx, const double* cy, double hwy, int d,
                          double eta) {
@@ -192,7 +192,7 @@ void oh2_tree_free(oh2_tree* t) {
 }
 
 /* sort a small list of cell indices by their level keys (insertion sort:
- * lists are at most a few hundred entries) — geometry.py:396-397 */
+ * lists are at most a few hundred entries) — geometry.py:333-334 */
 static void sort_by_key(int64_t* idx, int64_t n, const int64_t* keys) {
   for (int64_t i = 1; i < n; i++) {
     int64_t v = idx[i], kv = keys[v], j = i - 1;
@@ -204,7 +204,7 @@ static void sort_by_key(int64_t* idx, int64_t n, const int64_t* keys) {
   }
 }
 
-/* geometry.py:385 _annotate_level restricted to nonempty cells (empty cells
+/* geometry.py:322 _annotate_level restricted to nonempty cells (empty cells
  * have no points and no nonempty descendants, so they never contribute to
  * any candidate set, coupling or near-field block) */
 static void annotate_level(oh2_tree* t, int level) {
@@ -273,7 +273,7 @@ static void fill_ranges(const kpair* pr, int64_t npts, const int64_t* keys, int6
 
 int oh2_build_tree(const double* P, int64_t np, const double* Q, int64_t nq, int d, int shared,
                    int64_t nu, double eta, oh2_tree** out) {
-  /* geometry.py:298-303 */
+  /* geometry.py:235-240 */
   if (np == 0 || nq == 0) return fail("empty point set");
   if (nu < 1) return fail("invalid leaf capacity");
   if (!(eta > 0)) return fail("eta must be positive");
@@ -295,7 +295,7 @@ int oh2_build_tree(const double* P, int64_t np, const double* Q, int64_t nq, int
     memcpy(t->Q, Q, sizeof(double) * nq * d);
   }
 
-  /* geometry.py:306-310 root box */
+  /* geometry.py:243-247 root box */
   double lo[MAXD], hi[MAXD];
   for (int k = 0; k < d; k++) {
     lo[k] = INFINITY;
@@ -364,7 +364,7 @@ int oh2_build_tree(const double* P, int64_t np, const double* Q, int64_t nq, int
   int level = 0;
   int rc = 0;
   for (;;) {
-    /* geometry.py:327-330 */
+    /* geometry.py:264-267 */
     olevel* L = &t->lv[level];
     int64_t worst = 0;
     for (int64_t c = 0; c < L->n; c++) {
@@ -373,7 +373,7 @@ int oh2_build_tree(const double* P, int64_t np, const double* Q, int64_t nq, int
       if (w > worst) worst = w;
     }
     if (worst <= nu) break;
-    /* geometry.py:331-336 */
+    /* geometry.py:268-273 */
     double width = half * ldexp(1.0, -level);
     if (width / (2.0 * half) < WIDTH_UNDERFLOW) {
       for (int64_t c = 0; c < L->n; c++) {
@@ -384,11 +384,11 @@ int oh2_build_tree(const double* P, int64_t np, const double* Q, int64_t nq, int
       break;
     }
     if ((int64_t)(level + 1) * d >= 63) {
-      /* np.ravel_multi_index overflow in geometry.py:366 */
+      /* np.ravel_multi_index overflow in geometry.py:303 */
       rc = fail("invalid dims: array size defined by dims is larger than the maximum possible size.");
       break;
     }
-    /* geometry.py:338-342 bin refinement, exact reference arithmetic */
+    /* geometry.py:275-279 bin refinement, exact reference arithmetic */
     double w2 = 2.0 * width;
     for (int pass = 0; pass < (shared ? 1 : 2); pass++) {
       const double* pts = pass == 0 ? t->P : t->Q;
@@ -406,7 +406,7 @@ int oh2_build_tree(const double* P, int64_t np, const double* Q, int64_t nq, int
       rc = fail("tree too deep");
       break;
     }
-    /* geometry.py:365-374 grouping */
+    /* geometry.py:302-311 grouping */
     kpair* pp = (kpair*)xmalloc(sizeof(kpair) * np);
     for (int64_t i = 0; i < np; i++) {
       pp[i].key = ravel(bins_p + i * d, d, level);
@@ -527,7 +527,7 @@ int64_t oh2_tree_get(const oh2_tree* t, int level, int what, int64_t* dst) {
 }
 
 /* ------------------------------------------------------------------ */
-/* ACA: _core.pyx:184 aca_kernel                                       */
+/* ACA: _core.pyx:70 aca_kernel                                       */
 /* U, V kept column-major by rank (U[t*m+i], V[t*n+j]); the arithmetic  */
 /* order per entry is exactly the reference's.                         */
 /* ------------------------------------------------------------------ */
@@ -680,7 +680,7 @@ int64_t oh2_aca(int kind, double a, const double* X, int64_t m, const double* Y,
   return r.k;
 }
 
-/* aca.py:476 row_interpolator: P = U L^{-1}, L = tril(U[rp]); P[rp] = I.
+/* aca.py:297 row_interpolator: P = U L^{-1}, L = tril(U[rp]); P[rp] = I.
  * Uc column-major (Uc[t*m+i]); out row-major (m x k). */
 static void row_interp_cm(const double* Uc, int64_t m, int64_t k, const int64_t* rp, double* out) {
   for (int64_t i = 0; i < m; i++) {
@@ -697,7 +697,7 @@ static void row_interp_cm(const double* Uc, int64_t m, int64_t k, const int64_t*
   }
 }
 
-/* aca.py:490 col_interpolator: Q = V R^{-T}, R = triu(V[cp].T), unit diag;
+/* aca.py:311 col_interpolator: Q = V R^{-T}, R = triu(V[cp].T), unit diag;
  * Q[cp] = I.  Vc column-major; out row-major (n x k). */
 static void col_interp_cm(const double* Vc, int64_t n, int64_t k, const int64_t* cp, double* out) {
   for (int64_t j = 0; j < n; j++) {
@@ -1014,7 +1014,7 @@ void oh2_h2_stats(const oh2_h2* h, int64_t* evals_pivots, int64_t* evals_couplin
 }
 
 /* ------------------------------------------------------------------ */
-/* matvec: matvec.py:510 h2_matvec_reference (S and near-field blocks   */
+/* matvec: matvec.py:169 h2_matvec_reference (S and near-field blocks   */
 /* regenerated entry by entry instead of stored)                        */
 /* ------------------------------------------------------------------ */
 int oh2_matvec(const oh2_h2* h, const double* w, double* u, int64_t nrhs) {
@@ -1127,7 +1127,7 @@ int oh2_matvec(const oh2_h2* h, const double* w, double* u, int64_t nrhs) {
       }
     }
   }
-  /* near field (matvec.py:561-567) */
+  /* near field (matvec.py:220-226) */
   {
     const olevel* L = &t->lv[depth];
 #pragma omp parallel for schedule(dynamic, 16) num_threads(oh2_get_threads())

@@ -34,7 +34,7 @@ const char* oh2_last_error(void);
 void oh2_set_threads(int n);
 int oh2_get_threads(void);
 
-/* geometry.py:293 build_tree (+ geometry.py:385 _annotate_level) */
+/* geometry.py:230 build_tree (+ geometry.py:322 _annotate_level) */
 int oh2_build_tree(const double* P, int64_t np, const double* Q, int64_t nq, int d,
                    int shared, int64_t nu, double eta, oh2_tree** out);
 void oh2_tree_free(oh2_tree* t);
@@ -47,21 +47,21 @@ int64_t oh2_tree_ncells(const oh2_tree* t, int level);
  *       11 ch_ptr(n+1) 12 ch_idx ; returns element count, copies if dst */
 int64_t oh2_tree_get(const oh2_tree* t, int level, int what, int64_t* dst);
 
-/* geometry.py:210 boxes_admissible */
+/* geometry.py:147 boxes_admissible */
 int oh2_boxes_admissible(const double* cx, double hwx, const double* cy, double hwy, int d, double eta);
 
-/* _core.pyx:129 _kval + :152 _r2 ; _core.pyx:161 kernel_block */
+/* _core.pyx:15 _kval + :38 _r2 ; _core.pyx:47 kernel_block */
 double oh2_kval(int kind, double a, double r2);
 void oh2_kernel_block(int kind, double a, const double* X, int64_t m, const double* Y, int64_t n,
                       int d, double* out);
 
-/* _core.pyx:184 aca_kernel.  U (m x k) and V (n x k) row-major, rp/cp local
+/* _core.pyx:70 aca_kernel.  U (m x k) and V (n x k) row-major, rp/cp local
  * pivots.  Buffers must hold cap columns.  Returns rank k. */
 int64_t oh2_aca(int kind, double a, const double* X, int64_t m, const double* Y, int64_t n, int d,
                 double eps, int64_t cap, double* U, double* V, int64_t* rp, int64_t* cp,
                 int* converged, int64_t* nevals);
 
-/* aca.py:476 row_interpolator / aca.py:490 col_interpolator on factors from
+/* aca.py:297 row_interpolator / aca.py:311 col_interpolator on factors from
  * oh2_aca (row-major m x k / n x k).  out: row-major (rows x k). */
 void oh2_row_interpolator(const double* U, int64_t m, int64_t k, const int64_t* rp, double* out);
 void oh2_col_interpolator(const double* V, int64_t n, int64_t k, const int64_t* cp, double* out);
@@ -81,10 +81,10 @@ int64_t oh2_h2_get_interp(const oh2_h2* h, int level, int64_t cell, int which, i
 void oh2_h2_stats(const oh2_h2* h, int64_t* evals_pivots, int64_t* evals_couplings,
                   int64_t* evals_nearfield, int64_t* max_rank, int64_t* cells_visited);
 
-/* matvec.py:510 h2_matvec_reference with regenerated S and near-field blocks.
+/* matvec.py:169 h2_matvec_reference with regenerated S and near-field blocks.
  * w: n_sources x nrhs (row-major), u: n_targets x nrhs. */
 int oh2_matvec(const oh2_h2* h, const double* w, double* u, int64_t nrhs);
-/* matvec.py:574 dense_matvec */
+/* matvec.py:233 dense_matvec */
 void oh2_dense_matvec(int kind, double a, const double* P, int64_t np, const double* Q, int64_t nq,
                       int d, const double* w, double* u, int64_t nrhs);
 void oh2_dense_rows(int kind, double a, const double* P, const int64_t* rows, int64_t nrows,

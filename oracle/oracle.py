@@ -5,8 +5,8 @@ TEST INFRASTRUCTURE ONLY: imported by ``tests/``, ``__graft_entry__.smoke()``
 The product package ``paper_2203_14832_b200`` never imports this module.
 
 The oracle restates the reference h2cross algorithm for the hot path
-(geometry.py:293 build_tree, compress.py:216 select_pivots, _core.pyx:184
-aca_kernel, matvec.py:510 h2_matvec_reference); it is pinned against golden
+(geometry.py:230 build_tree, compress.py:216 select_pivots, _core.pyx:70
+aca_kernel, matvec.py:169 h2_matvec_reference); it is pinned against golden
 vectors produced by the reference itself (tests/golden/make_golden.py).
 """
 
@@ -197,7 +197,7 @@ class OH2:
 
 
 def aca(kind, a, X, Y, eps, cap=None):
-    """Restated _core.pyx:184 aca_kernel: returns (U, V, rp, cp, converged, nevals)."""
+    """Restated _core.pyx:70 aca_kernel: returns (U, V, rp, cp, converged, nevals)."""
     X = np.ascontiguousarray(X, dtype=np.float64)
     Y = np.ascontiguousarray(Y, dtype=np.float64)
     m, n, d = X.shape[0], Y.shape[0], X.shape[1]

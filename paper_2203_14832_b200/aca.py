@@ -1,7 +1,7 @@
 """Partially pivoted adaptive cross approximation (aca.py of h2cross).
 
 ``partial_aca`` over a ``KernelOracle`` runs the GPU kernel
-(h2b_aca_kernel, replacing _accel/_core.pyx:184 aca_kernel): one CTA, the
+(h2b_aca_kernel, replacing _accel/_core.pyx:70 aca_kernel): one CTA, the
 reference's pivot rules and exact residual arithmetic, so pivots, U and V
 match the reference bit-for-bit for the IEEE-exact kernels.
 
@@ -28,7 +28,7 @@ PIVOT_RTOL = 1e-14
 
 @dataclass
 class ACAResult:
-    """Low-rank factors, pivots, and the pivot-block triangular factors (aca.py:219)."""
+    """Low-rank factors, pivots, and the pivot-block triangular factors (aca.py:41)."""
 
     row_pivots: np.ndarray
     col_pivots: np.ndarray
@@ -47,7 +47,7 @@ class ACAResult:
 
 
 class EntryOracle:
-    """Adapts a scalar ``f(i, j)`` entry function (aca.py:239)."""
+    """Adapts a scalar ``f(i, j)`` entry function (aca.py:60)."""
 
     def __init__(self, fn):
         self.fn = fn
@@ -60,7 +60,7 @@ class EntryOracle:
 
 
 class KernelOracle:
-    """Entry oracle K(p_i, q_j) over a point cloud, counted in EVALS (aca.py:252)."""
+    """Entry oracle K(p_i, q_j) over a point cloud, counted in EVALS (aca.py:73)."""
 
     def __init__(self, kernel: KernelSpec, cloud):
         self.kernel = kernel
@@ -104,7 +104,7 @@ def _finish(rows, cols, U, V, rp, cp, k, converged, n_evals=0):
 
 
 def aca_kernel(kind: int, a: float, X: np.ndarray, Y: np.ndarray, eps: float, cap: int):
-    """GPU twin of _core.pyx:184 aca_kernel: (U, V, rp, cp, converged, nevals)."""
+    """GPU twin of _core.pyx:70 aca_kernel: (U, V, rp, cp, converged, nevals)."""
     X = _lib.f64(X)
     Y = _lib.f64(Y)
     m, n = X.shape[0], Y.shape[0]
@@ -126,7 +126,7 @@ def aca_kernel(kind: int, a: float, X: np.ndarray, Y: np.ndarray, eps: float, ca
 
 
 def partial_aca(rows, cols, oracle, epsilon: float, max_rank: int | None = None) -> ACAResult:
-    """Run partially pivoted ACA on the block A[rows, cols] (aca.py:301).
+    """Run partially pivoted ACA on the block A[rows, cols] (aca.py:122).
 
     ``oracle`` must be a ``KernelOracle`` over a built-in kernel; Python
     callables cannot run on the GPU engine and are refused.
@@ -153,7 +153,7 @@ def partial_aca(rows, cols, oracle, epsilon: float, max_rank: int | None = None)
 
 
 def apply_pivot_inverse(result: ACAResult, rhs: np.ndarray) -> np.ndarray:
-    """Apply A[tau, sigma]^{-1} to ``rhs`` via the stored triangular factors (aca.py:443)."""
+    """Apply A[tau, sigma]^{-1} to ``rhs`` via the stored triangular factors (aca.py:264)."""
     low, up = result.pivot_lu
     k = result.rank
     rhs = np.asarray(rhs, dtype=np.float64)
@@ -176,7 +176,7 @@ def apply_pivot_inverse(result: ACAResult, rhs: np.ndarray) -> np.ndarray:
 
 
 def row_interpolator(result: ACAResult) -> np.ndarray:
-    """A[:, sigma] A[tau, sigma]^{-1} == U L^{-1}, pivot rows pinned to I (aca.py:476)."""
+    """A[:, sigma] A[tau, sigma]^{-1} == U L^{-1}, pivot rows pinned to I (aca.py:297)."""
     low, _ = result.pivot_lu
     k = result.rank
     if k == 0:
@@ -187,7 +187,7 @@ def row_interpolator(result: ACAResult) -> np.ndarray:
 
 
 def col_interpolator(result: ACAResult) -> np.ndarray:
-    """(A[tau, sigma]^{-1} A[tau, :])^T == V R^{-T}, pivot rows pinned to I (aca.py:490)."""
+    """(A[tau, sigma]^{-1} A[tau, :])^T == V R^{-T}, pivot rows pinned to I (aca.py:311)."""
     _, up = result.pivot_lu
     k = result.rank
     if k == 0:

@@ -101,7 +101,7 @@ void ensure_host_level(h2b_tree* T, int level) {
     for (int64_t i = 0; i < n; i++) {
       int64_t c = perm[i];
       std::copy(pm.begin() + ptr[c], pm.begin() + ptr[c + 1], oidx.begin() + optr[i]);
-      std::sort(oidx.begin() + optr[i], oidx.begin() + optr[i + 1]);  // geometry.py:289 np.sort
+      std::sort(oidx.begin() + optr[i], oidx.begin() + optr[i + 1]);  // geometry.py:226 np.sort
     }
   };
   ranges(tptr, tperm, H.t_ptr, H.t_idx);

@@ -1,8 +1,8 @@
 // common.cuh — shared device helpers for the B200 NNCA / H2 engine.
 //
 // Two families of kernel evaluators:
-//   * kval_exact / r2_exact: the reference's arithmetic (_core.pyx:129 _kval,
-//     :152 _r2) with every rounding pinned by __d*_rn intrinsics so nvcc
+//   * kval_exact / r2_exact: the reference's arithmetic (_core.pyx:15 _kval,
+//     :38 _r2) with every rounding pinned by __d*_rn intrinsics so nvcc
 //     cannot contract into FMAs.  Used wherever results feed a discrete
 //     decision (ACA pivot search) or are compared bit-for-bit.
 //   * the fast evaluators in interact.cuh: FMA-contracted distance, MUFU
@@ -75,7 +75,7 @@ __device__ __forceinline__ double kval_exact(int kind, double a, double r2) {
   }
 }
 
-// sum_k (x_k - y_k)^2 accumulated left to right from 0.0, no FMA (_core.pyx:152)
+// sum_k (x_k - y_k)^2 accumulated left to right from 0.0, no FMA (_core.pyx:38)
 template <int D>
 __device__ __forceinline__ double r2_exact(const double* x, const double* y) {
   double acc = 0.0;

@@ -9,7 +9,7 @@
 //     contiguous range [ch_ptr[c], ch_ptr[c+1]) of the next level — so every
 //     M2M/L2L operand is a contiguous slice.
 //   * lists: neighbour / interaction lists in CSR, each list sorted by the
-//     reference's row-major multi-index key (geometry.py:396-397) because the
+//     reference's row-major multi-index key (geometry.py:333-334) because the
 //     order of the ACA candidate columns depends on it.
 //   * H2: per level, pivot coordinates (SoA), pivot global indices, and the
 //     interpolation operators of every cell, column-major (row index

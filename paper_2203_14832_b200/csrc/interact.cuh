@@ -652,13 +652,8 @@ void pack_coords_d(const DevH2& h, cudaStream_t s) {
 // [2^-100, 2^100].  Admissible cells at level l satisfy diam <= eta * gap
 // (geometry.py:147), so r >= 2 hw_l sqrt(d) / eta >= 2 hw_depth sqrt(d) / eta;
 // in the shifted frame every term of r^2 is bounded by (4 sqrt(d) half)^2.
-// H2B_F32SEED=0 forces the cubic FP64-seeded path.
+// Otherwise (tests scale the geometry by 2^+-100) the cubic FP64-seeded path runs.
 inline bool f32seed_ok(const DevH2& h) {
-  static const int env = [] {
-    const char* e = getenv("H2B_F32SEED");
-    return e ? atoi(e) : 1;
-  }();
-  if (!env) return false;
   const DevTree& t = *h.t;
   const double hw = t.half * std::ldexp(1.0, -t.depth);
   const double rmin = 2.0 * hw * std::sqrt((double)t.d) / (t.eta > 0 ? t.eta : 1.0);

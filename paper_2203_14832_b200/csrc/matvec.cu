@@ -1,5 +1,5 @@
-// matvec.cu — level-batched H2 matrix-vector product (matvec.py:483 h2_matvec,
-// the five passes of matvec.py:510 h2_matvec_reference), FP64 throughout.
+// matvec.cu — level-batched H2 matrix-vector product (matvec.py:142 h2_matvec,
+// the five passes of matvec.py:169 h2_matvec_reference), FP64 throughout.
 //
 // The coupling blocks S_{X,Y} = K(t_in^X, s_out^Y) and the near-field blocks
 // are NOT stored (the reference stores both): both are regenerated in
@@ -637,10 +637,7 @@ void build_tabs(DevH2& h, int64_t R, cudaStream_t s) {
     h.m_sb.resize(L + 2);
     h.m_end.resize(L + 2);
     h.m_cnt.resize(L + 2);
-    static const int merge = [] {
-      const char* e = getenv("H2B_MERGE_MEMBERS");
-      return e ? atoi(e) : 1;
-    }();
+    const int merge = 1;  // adjacent record ranges merged into one member (one TMA copy per run)
     std::vector<int> ids;
     for (int l = 2; l <= L; l++) ids.push_back(l);
     ids.push_back(L + 1);  // the near field (also when the tree has fewer than two levels)
@@ -755,11 +752,7 @@ void ensure_scratch(DevH2& h, int64_t R, cudaStream_t s) {
       const int64_t nr_sum = (int64_t)(h.symmetric ? HL.pmat.n : HL.qmat.n);  // sum over cells of nr * k
       const int64_t nr_avg = rows ? nr_sum / rows : 0;
       h.up_sg[l] = up_group(rows, nr_avg);
-      static const int cap = [] {  // tuning: cap on the lanes per row (H2B_UP_SG_CAP)
-        const char* e = getenv("H2B_UP_SG_CAP");
-        return e ? atoi(e) : 16;
-      }();
-      while (h.up_sg[l] > std::max(cap, 1)) h.up_sg[l] /= 2;
+      while (h.up_sg[l] > 16) h.up_sg[l] /= 2;
     }
     const DevLevel& Lf = T.lv[T.depth];
     h.own_t.alloc(std::max<int64_t>(T.np, 1), &h.mem);
@@ -941,7 +934,7 @@ void matvec(DevH2& h, const double* w, double* u, int64_t R, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------------
-// dense oracles (matvec.py:574 dense_matvec) and kernel blocks
+// dense oracles (matvec.py:233 dense_matvec) and kernel blocks
 // ---------------------------------------------------------------------
 namespace {
 

@@ -1,6 +1,6 @@
 // nnca.cu — NNCA construction on the GPU (compress.py:216 select_pivots,
 // compress.py:285 assemble) with the partially pivoted ACA of
-// _accel/_core.pyx:184 run as one CTA per cell, level-batched bottom-up.
+// _accel/_core.pyx:70 run as one CTA per cell, level-batched bottom-up.
 //
 // Pivot parity: every residual entry is formed with the reference's exact
 // operation order (kernel value, then `acc -= U[i,t] * V[j,t]` for t =
@@ -10,7 +10,7 @@
 // reduction (different summation order), which can flip the stop decision
 // only when ||u_k|| ||v_k|| lands within roundoff of eps ||A_k||_F.
 //
-// Interpolation operators (aca.py:476 row_interpolator, :490
+// Interpolation operators (aca.py:297 row_interpolator, :311
 // col_interpolator) are back-substitutions against the pivot rows of U / V
 // — the ACA byproduct, no further kernel evaluations (paper Remark 2).
 #include <cub/cub.cuh>
@@ -38,12 +38,6 @@ namespace {
 #endif
 #ifndef H2B_ACA_TB
 #define H2B_ACA_TB 4  // residual rows per load batch in the fused row pass
-#endif
-#ifndef H2B_ACA_WMINB
-#define H2B_ACA_WMINB 2
-#endif
-#ifndef H2B_ACA_WCPT
-#define H2B_ACA_WCPT 2
 #endif
 #ifndef H2B_ACA_SLAB_GB
 #define H2B_ACA_SLAB_GB 24
@@ -156,7 +150,7 @@ __device__ int64_t block_min(int64_t x, RedScratch& rs) {
   return rs.bi;
 }
 
-// _core.pyx:184-305, one CTA per cell
+// _core.pyx:70-191, one CTA per cell
 template <int D, int NT>
 __global__ void __launch_bounds__(NT, (2048 / NT / 2) > 0 ? (2048 / NT / 2) : 1) aca_kernel(AcaArgs A) {
   constexpr int ACA_THREADS = NT;
@@ -369,33 +363,6 @@ __global__ void __launch_bounds__(NT, (2048 / NT / 2) > 0 ? (2048 / NT / 2) : 1)
   }
 }
 
-// aca.py:476 row_interpolator: P = U L^{-1}, L[t][s] = U[rp[t], s]; P[rp] = I.
-// which==1: aca.py:490 col_interpolator: Q = V R^{-T}, R unit upper, Q[cp] = I.
-__global__ void interp_kernel(int which, int64_t cell0, const int64_t* __restrict__ rows_of,
-                              const int64_t* __restrict__ rank, const double* __restrict__ W,
-                              const int64_t* __restrict__ w_off, const int64_t* __restrict__ piv_loc,
-                              const int64_t* __restrict__ piv_off, double* __restrict__ out,
-                              const int64_t* __restrict__ out_off) {
-  const int64_t cell = cell0 + blockIdx.x;
-  const int64_t m = rows_of[cell], k = rank[cell];
-  if (k == 0 || m == 0) return;
-  const double* F = W + w_off[cell];
-  const int64_t* pv = piv_loc + piv_off[cell];
-  double* P = out + out_off[cell];
-  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
-    for (int64_t s = k - 1; s >= 0; s--) {
-      const double* Fs = F + s * m;
-      double acc = Fs[i];
-      for (int64_t t = s + 1; t < k; t++) acc -= P[t * m + i] * Fs[pv[t]];
-      P[s * m + i] = which == 0 ? acc / Fs[pv[s]] : acc;
-    }
-  }
-  __syncthreads();
-  for (int64_t q = threadIdx.x; q < k * k; q += blockDim.x) {
-    int64_t t = q / k, s = q % k;
-    P[s * m + pv[t]] = (s == t) ? 1.0 : 0.0;
-  }
-}
 
 // ---------------------------------------------------------------------
 // candidate set sizing / gathering (compress.py:159 candidate_sets)
@@ -534,7 +501,7 @@ DBuf<T> upload(const std::vector<T>& h, cudaStream_t s, MemStats* ms = nullptr) 
 // stays in the 126 MB L2: the ACA re-reads V (k x n) at every step, which in
 // a one-CTA-per-cell launch (thousands of cells resident) went to DRAM.
 // The far candidates of a cell are gathered from its interaction list into
-// the slab once, and the interpolation operator (aca.py:476 / :490) is
+// the slab once, and the interpolation operator (aca.py:297 / :311) is
 // formed right after the ACA from the same slab.  Pivot arithmetic is
 // unchanged (reference operation order, see aca_kernel).
 // ---------------------------------------------------------------------
@@ -985,371 +952,6 @@ __global__ void __launch_bounds__(NT, MB) aca_cells(CellJob J) {
   }
 }
 
-// ---------------------------------------------------------------------
-// Warp-per-cell ACA (the default setup path).  Every warp is an independent
-// persistent worker with its own global slab (U, V, far candidates, flags)
-// and a few cap-sized vectors in shared memory: no block barriers, and with
-// tens of resident warps per SM the dependent phases of one cell's ACA step
-// (row pass -> argmax -> column pass -> norms) overlap with other cells'
-// memory traffic.  Arithmetic identical to aca_cells (reference operation
-// order for every residual; fused row pass that also normalises the previous
-// row and forms its cross products; speculative stopping test).
-// ---------------------------------------------------------------------
-template <int D, int CPT>
-__global__ void __launch_bounds__(256, H2B_ACA_WMINB) aca_warps(CellJob J) {
-  constexpr int WPB = 8;  // warps per block
-  extern __shared__ double sm[];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int64_t gw = (int64_t)blockIdx.x * WPB + wib;
-  double* urow = sm + (int64_t)wib * 5 * J.cap_max;
-  double* vcol = urow + J.cap_max;
-  double* crossv = urow + 2 * J.cap_max;
-  double* crossu = urow + 3 * J.cap_max;
-  double* crosspart = urow + 4 * J.cap_max;
-  double* base = J.ws + gw * J.ws_doubles;
-  double* U = base;
-  double* V = U + J.u_slab;
-  double* FC = V + J.v_slab;
-  int64_t* FG = reinterpret_cast<int64_t*>(FC + D * J.f_max);
-  int64_t* RP = FG + J.f_max;
-  int64_t* CP = RP + J.cap_max;
-  unsigned char* flags = reinterpret_cast<unsigned char*>(CP + J.cap_max);
-  for (;;) {
-    unsigned long long q = 0;
-    if (lane == 0) q = atomicAdd(J.counter, 1ull);
-    q = __shfl_sync(0xffffffffu, q, 0);
-    if (q >= (unsigned long long)J.ncell) break;
-    const int64_t cell = J.order[q];
-    // ---- own range and far candidates (gathered into the slab, 32 members per round) ----
-    int64_t ob, oe;
-    src_range(J.own, cell, ob, oe);
-    const int64_t own_n = oe - ob;
-    const int64_t lb = J.il_ptr[cell], le = J.il_ptr[cell + 1];
-    int64_t far_n = 0;
-    for (int64_t q0 = lb; q0 < le; q0 += 32) {
-      const int nm = (int)(le - q0 < 32 ? le - q0 : 32);
-      int64_t b = 0, len = 0;
-      if (lane < nm) {
-        int64_t e;
-        src_range(J.far, J.il_idx[q0 + lane], b, e);
-        len = e - b;
-      }
-      int64_t v = len;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const long long n2 = __shfl_up_sync(0xffffffffu, (long long)v, o);
-        if (lane >= o) v += n2;
-      }
-      const int64_t tot = __shfl_sync(0xffffffffu, (long long)v, 31);
-      const int64_t myoff = far_n + v - len;
-      for (int mm = 0; mm < nm; mm++) {
-        const int64_t mb = __shfl_sync(0xffffffffu, (long long)b, mm);
-        const int64_t mo = __shfl_sync(0xffffffffu, (long long)myoff, mm);
-        const int64_t ml = __shfl_sync(0xffffffffu, (long long)len, mm);
-        for (int64_t e = lane; e < ml; e += 32) {
-#pragma unroll
-          for (int k = 0; k < D; k++) FC[k * J.f_max + mo + e] = J.far.coords[k * J.far.ld + mb + e];
-          FG[mo + e] = J.far.gidx[mb + e];
-        }
-      }
-      far_n += tot;
-    }
-    __syncwarp();
-    const int64_t m = J.rows_far ? far_n : own_n;
-    const int64_t n = J.rows_far ? own_n : far_n;
-    const int64_t cap = J.caps[cell];
-    auto rowc = [&](int k, int64_t i) -> double {
-      return J.rows_far ? FC[k * J.f_max + i] : J.own.coords[k * J.own.ld + ob + i];
-    };
-    auto colc = [&](int k, int64_t j) -> double {
-      return J.rows_far ? J.own.coords[k * J.own.ld + ob + j] : FC[k * J.f_max + j];
-    };
-    if (m == 0 || n == 0 || cap == 0) {
-      if (lane == 0) {
-        J.rank[cell] = 0;
-        J.conv[cell] = (m == 0 || n == 0) ? 1 : 0;
-        J.nevals[cell] = 0;
-      }
-      continue;
-    }
-    unsigned char* ru = flags;
-    unsigned char* cu = flags + m;
-    for (int64_t i = lane; i < m + n; i += 32) ru[i] = 0;
-    const int64_t full = m < n ? m : n;
-    int64_t k = 0, trial = 0, nev = 0;
-    double norm2 = 0.0;
-    int64_t converged = 1;
-    bool pend = false;
-    double piv_prev = 1.0, u2_prev = 0.0;
-    const int ni = (int)n;
-    __syncwarp();
-    auto finish_row = [&](int r, bool need_cross) -> double {
-      double v2p = 0.0;
-      double* Vr = V + (int64_t)r * n;
-      for (int j = lane; j < ni; j += 32) {
-        const double v = __ddiv_rn(Vr[j], piv_prev);
-        Vr[j] = v;
-        v2p += v * v;
-      }
-      __syncwarp();
-      if (need_cross)
-        for (int t = 0; t < r; t++) {
-          const double* Vt = V + (int64_t)t * n;
-          double s0 = 0.0;
-          for (int j = lane; j < ni; j += 32) s0 = fma(Vt[j], Vr[j], s0);
-          s0 = warp_sum(s0);
-          if (lane == 0) crossv[t] = s0;
-        }
-      __syncwarp();
-      return warp_sum(v2p);
-    };
-    for (;;) {
-      bool exhausted = false, stop_prev = false, fuse = pend;
-      double best;
-      int64_t bj;
-      for (;;) {
-        if (lane == 0) ru[trial] = 1;
-        for (int64_t t = lane; t < k; t += 32) urow[t] = U[t * m + trial];
-        if (fuse)
-          for (int64_t t = lane; t < k; t += 32) crosspart[t] = 0.0;
-        double xl[D];
-#pragma unroll
-        for (int qd = 0; qd < D; qd++) xl[qd] = rowc(qd, trial);
-        __syncwarp();
-        best = -1.0;
-        bj = -1;
-        const int ki = (int)k;
-        const int kf = fuse ? ki - 1 : ki;
-        double v2p = 0.0;
-        double* Vlast = V + (int64_t)(ki - 1) * n;
-        for (int jb = 0; jb < ni; jb += CPT * 32) {
-          const int j0 = jb + lane;
-          double acc[CPT], vl[CPT], y[CPT][D], raw[CPT];
-          int jc[CPT];
-#pragma unroll
-          for (int c = 0; c < CPT; c++) {
-            const int jj = j0 + c * 32;
-            jc[c] = jj < ni ? jj : 0;
-#pragma unroll
-            for (int qd = 0; qd < D; qd++) y[c][qd] = colc(qd, jc[c]);
-            raw[c] = fuse ? Vlast[jc[c]] : 0.0;
-          }
-#pragma unroll
-          for (int c = 0; c < CPT; c++) {
-            const int jj = j0 + c * 32;
-            acc[c] = jj < ni ? kval_exact(J.kind, J.a, r2_exact<D>(xl, y[c])) : 0.0;  // no work on padding
-            vl[c] = 0.0;
-            if (fuse && jj < ni) {
-              vl[c] = __ddiv_rn(raw[c], piv_prev);
-              Vlast[jj] = vl[c];
-              v2p += vl[c] * vl[c];
-            }
-          }
-          const double* Vt = V;
-          if (fuse) {
-            for (int t0 = 0; t0 < kf; t0 += 4, Vt += 4 * (int64_t)n) {
-              double v[4][CPT];
-              const bool full4 = t0 + 4 <= kf;
-#pragma unroll
-              for (int tt = 0; tt < 4; tt++)
-#pragma unroll
-                for (int c = 0; c < CPT; c++)
-                  v[tt][c] = (full4 || t0 + tt < kf) ? Vt[(int64_t)tt * n + jc[c]] : 0.0;
-              double p[4];
-#pragma unroll
-              for (int tt = 0; tt < 4; tt++) {
-                p[tt] = 0.0;
-                if (full4 || t0 + tt < kf) {
-                  const double ut = urow[t0 + tt];
-#pragma unroll
-                  for (int c = 0; c < CPT; c++) {
-                    acc[c] = __dsub_rn(acc[c], __dmul_rn(ut, v[tt][c]));
-                    p[tt] = fma(v[tt][c], vl[c], p[tt]);
-                  }
-                }
-              }
-              const bool b4 = lane & 16, b3 = lane & 8;
-              double k0 = b4 ? p[2] : p[0], k1 = b4 ? p[3] : p[1];
-              k0 += __shfl_xor_sync(0xffffffffu, b4 ? p[0] : p[2], 16);
-              k1 += __shfl_xor_sync(0xffffffffu, b4 ? p[1] : p[3], 16);
-              double kk = b3 ? k1 : k0;
-              kk += __shfl_xor_sync(0xffffffffu, b3 ? k0 : k1, 8);
-              kk += __shfl_xor_sync(0xffffffffu, kk, 4);
-              kk += __shfl_xor_sync(0xffffffffu, kk, 2);
-              kk += __shfl_xor_sync(0xffffffffu, kk, 1);
-              const int tq = t0 + ((lane >> 3) & 3);
-              if ((lane & 7) == 0 && tq < kf) crosspart[tq] += kk;
-            }
-#pragma unroll
-            for (int c = 0; c < CPT; c++) acc[c] = __dsub_rn(acc[c], __dmul_rn(urow[ki - 1], vl[c]));
-          } else {
-            int t = 0;
-            for (; t + 4 <= ki; t += 4, Vt += 4 * (int64_t)n) {
-              double v[4][CPT];
-#pragma unroll
-              for (int tt = 0; tt < 4; tt++)
-#pragma unroll
-                for (int c = 0; c < CPT; c++) v[tt][c] = Vt[(int64_t)tt * n + jc[c]];
-#pragma unroll
-              for (int tt = 0; tt < 4; tt++) {
-                const double ut = urow[t + tt];
-#pragma unroll
-                for (int c = 0; c < CPT; c++) acc[c] = __dsub_rn(acc[c], __dmul_rn(ut, v[tt][c]));
-              }
-            }
-            for (; t < ki; t++, Vt += ni) {
-              const double ut = urow[t];
-#pragma unroll
-              for (int c = 0; c < CPT; c++) acc[c] = __dsub_rn(acc[c], __dmul_rn(ut, Vt[jc[c]]));
-            }
-          }
-#pragma unroll
-          for (int c = 0; c < CPT; c++) {
-            const int jj = j0 + c * 32;
-            if (jj < ni) {
-              V[(int64_t)k * n + jj] = acc[c];
-              if (!cu[jj]) {
-                const double val = fabs(acc[c]);
-                if (val > best) {
-                  best = val;
-                  bj = jj;
-                }
-              }
-            }
-          }
-        }
-        if (bj < 0) best = -1.0;
-        warp_argmax(best, bj);
-        __syncwarp();
-        if (fuse) {
-          for (int t = lane; t < kf; t += 32) crossv[t] = crosspart[t];
-          const double v2 = warp_sum(v2p);
-          __syncwarp();
-          for (int t = 0; t < kf; t++) norm2 += 2.0 * crossu[t] * crossv[t];
-          norm2 += u2_prev * v2;
-          pend = false;
-          fuse = false;
-          if (u2_prev * v2 <= J.eps2 * (norm2 > 0.0 ? norm2 : 0.0)) {
-            stop_prev = true;
-            break;
-          }
-        }
-        nev += n;
-        if (best > 0.0) break;
-        int64_t first = INT64_MAX;
-        for (int64_t i = lane; i < m; i += 32)
-          if (!ru[i] && i < first) first = i;
-        first = warp_min_i64(first);
-        if (first == INT64_MAX) {
-          exhausted = true;
-          break;
-        }
-        trial = first;
-        __syncwarp();
-      }
-      if (stop_prev || exhausted) break;
-      const double piv = V[k * n + bj];
-      double yl[D];
-#pragma unroll
-      for (int qd = 0; qd < D; qd++) yl[qd] = colc(qd, bj);
-      for (int64_t t = lane; t < k; t += 32) vcol[t] = V[t * n + bj];
-      __syncwarp();
-      if (lane == 0) cu[bj] = 1;
-      double u2p = 0.0;
-      for (int64_t i = lane; i < m; i += 32) {
-        double xq[D];
-#pragma unroll
-        for (int qd = 0; qd < D; qd++) xq[qd] = rowc(qd, i);
-        double acc = kval_exact(J.kind, J.a, r2_exact<D>(xq, yl));
-        for (int64_t t = 0; t < k; t++) acc = __dsub_rn(acc, __dmul_rn(U[t * m + i], vcol[t]));
-        U[k * m + i] = acc;
-        u2p += acc * acc;
-      }
-      nev += m;
-      __syncwarp();
-      for (int64_t t = 0; t < k; t++) {
-        double sacc = 0.0;
-        const double* Ut = U + t * m;
-        const double* Uk = U + k * m;
-        for (int64_t i = lane; i < m; i += 32) sacc += Ut[i] * Uk[i];
-        sacc = warp_sum(sacc);
-        if (lane == 0) crossu[t] = sacc;
-      }
-      const double u2 = warp_sum(u2p);
-      if (lane == 0) {
-        RP[k] = trial;
-        CP[k] = bj;
-      }
-      __syncwarp();
-      piv_prev = piv;
-      u2_prev = u2;
-      k += 1;
-      if (k == full) {
-        finish_row((int)k - 1, false);
-        break;
-      }
-      if (k == cap) {
-        const double v2 = finish_row((int)k - 1, true);
-        for (int64_t t = 0; t < k - 1; t++) norm2 += 2.0 * crossu[t] * crossv[t];
-        norm2 += u2 * v2;
-        if (!(u2 * v2 <= J.eps2 * (norm2 > 0.0 ? norm2 : 0.0))) converged = 0;
-        break;
-      }
-      best = -1.0;
-      int64_t bi = -1;
-      const double* Uk = U + (k - 1) * m;
-      for (int64_t i = lane; i < m; i += 32)
-        if (!ru[i]) {
-          const double val = fabs(Uk[i]);
-          if (val > best) {
-            best = val;
-            bi = i;
-          }
-        }
-      warp_argmax(best, bi);
-      if (bi < 0) {
-        finish_row((int)k - 1, false);
-        break;
-      }
-      trial = bi;
-      pend = true;
-      __syncwarp();
-    }
-    __syncwarp();
-    const int64_t po = J.piv_off[cell];
-    if (lane == 0) {
-      J.rank[cell] = k;
-      J.conv[cell] = converged;
-      J.nevals[cell] = nev;
-    }
-    for (int64_t t = lane; t < k; t += 32) {
-      const int64_t r = RP[t], c = CP[t];
-      J.tpiv[po + t] = J.rows_far ? FG[r] : J.own.gidx[ob + r];
-      J.spiv[po + t] = J.rows_far ? J.own.gidx[ob + c] : FG[c];
-    }
-    if (k > 0) {  // interpolation operator (interp_kernel arithmetic)
-      const int64_t rows = J.which == 0 ? m : n;
-      const double* F = J.which == 0 ? U : V;
-      const int64_t* pv = J.which == 0 ? RP : CP;
-      double* P = J.mat + J.mat_off[cell];
-      for (int64_t i = lane; i < rows; i += 32) {
-        for (int64_t sI = k - 1; sI >= 0; sI--) {
-          const double* Fs = F + sI * rows;
-          double acc = Fs[i];
-          for (int64_t t = sI + 1; t < k; t++) acc -= P[t * rows + i] * Fs[pv[t]];
-          P[sI * rows + i] = J.which == 0 ? acc / Fs[pv[sI]] : acc;
-        }
-      }
-      __syncwarp();
-      for (int64_t qq = lane; qq < k * k; qq += 32) {
-        const int64_t t = qq / k, sI = qq % k;
-        P[sI * rows + pv[t]] = (sI == t) ? 1.0 : 0.0;
-      }
-    }
-    __syncwarp();
-  }
-}
-
 template <int D, int NT>
 void set_aca_smem(size_t bytes) {
   static size_t done = 0;
@@ -1517,11 +1119,6 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
     int per = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, nt, smem));
     int64_t gmax = (int64_t)nsm * std::max(per, 1);
-    static const double gfrac = [] {
-      const char* e = getenv("H2B_ACA_GRID_FRAC");  // tuning: fraction of the SMs given to V-in-slab launches
-      return e ? atof(e) : 1.0;
-    }();
-    if (!vsmem && gfrac > 0 && gfrac < 1) gmax = std::max<int64_t>(1, (int64_t)(gmax * gfrac));
     int64_t grid = std::min<int64_t>((int64_t)cells.size(), gmax);
     J.ncell = (int64_t)cells.size();
     J.order = d_cells.get();
@@ -1596,48 +1193,11 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
 #endif
     }
   };
-#ifdef H2B_ACA_WARPS
-  {
-    // warp-per-cell workers (alternative; measured slower than the block workers on the sphere headline); concurrent warps bounded by the slab budget
-    auto kern = aca_warps<D, H2B_ACA_WCPT>;
-    int64_t us = 1, vs = 1;
-    for (int64_t c = 0; c < n; c++) {
-      us = std::max(us, caph[c] * mh[c]);
-      vs = std::max(vs, caph[c] * nh[c]);
-    }
-    J.u_slab = us;
-    J.v_slab = vs;
-    J.n_max = n_max;
-    int64_t ws = us + vs + D * f_max + f_max + 2 * cap_max + (m_max + n_max + 7) / 8 + 1;
-    ws = (ws + 31) / 32 * 32;
-    const size_t smem = (size_t)8 * 5 * cap_max * sizeof(double);
-    if (smem > 220 * 1024) throw std::runtime_error("ACA rank cap too large for shared memory");
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 256, smem));
-    const int64_t budget = (int64_t)H2B_ACA_SLAB_GB << 27;  // doubles
-    int64_t blocks = std::min<int64_t>((int64_t)nsm * std::max(per, 1), (n + 7) / 8);
-    blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, budget / (8 * ws)));
-    double* wsbuf = aca_arena((size_t)(blocks * 8 * ws), s);
-    DBuf<unsigned long long> counter;
-    counter.alloc(1);
-    CK(cudaMemsetAsync(counter.get(), 0, sizeof(unsigned long long), s));
-    J.ncell = n;
-    J.order = d_order_all.get();
-    J.ws = wsbuf;
-    J.ws_doubles = ws;
-    J.counter = counter.get();
-    kern<<<(unsigned)blocks, 256, smem, s>>>(J);
-    CKL();
-    CK(cudaStreamSynchronize(s));
-  }
-#else
   // V in shared memory: one 512-thread CTA per SM; V in the slab: H2B_ACA_NT threads x H2B_ACA_MINB CTAs
   // per SM (several cells in flight per SM hide the row pass's memory latency)
   launch(aca_cells<D, H2B_ACA_NT_S, CPT, true, true, 1>, H2B_ACA_NT_S, small, d_small, true, true);
   launch(aca_cells<D, NT, CPT, false, true, H2B_ACA_MINB>, NT, mid, d_mid, false, true);
   launch(aca_cells<D, NT, CPT, false, false, H2B_ACA_MINB>, NT, large, d_large, false, false);
-#endif
   CK(cudaStreamSynchronize(s));
   const auto wall3 = std::chrono::steady_clock::now();
   R.rank_h = to_host(R.rank.get(), n, s);
@@ -1814,7 +1374,7 @@ std::unique_ptr<DevH2> assemble(const DevTree& t, int kind, double a, double eps
   }
 }
 
-// Single-block ACA for the drop-in partial_aca path (_core.pyx:184).
+// Single-block ACA for the drop-in partial_aca path (_core.pyx:70).
 void aca_single(int kind, double a, const double* X, int64_t m, const double* Y, int64_t n, int d, double eps,
                 int64_t cap, double* U, double* V, int64_t* rp, int64_t* cp, int* conv, int64_t* nevals,
                 int64_t* rank) {

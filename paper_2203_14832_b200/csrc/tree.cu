@@ -1,5 +1,5 @@
-// tree.cu — GPU uniform 2^d tree build (geometry.py:293 build_tree) and
-// neighbour / interaction lists (geometry.py:385 _annotate_level).
+// tree.cu — GPU uniform 2^d tree build (geometry.py:230 build_tree) and
+// neighbour / interaction lists (geometry.py:322 _annotate_level).
 //
 // Bit-exactness: a point's cell at every level comes from the reference's
 // own recurrence  bin <- 2*bin + (p > lo0 + (bin + 0.5) * (2*width))  with
@@ -61,7 +61,7 @@ struct BinParams {
   double w2[64];  // 2 * (half * 2^-l): width of the level-l cell being split
 };
 
-// geometry.py:338-342 iterated Lmax times; code packs dim 0 as the most
+// geometry.py:275-279 iterated Lmax times; code packs dim 0 as the most
 // significant bit of every level group (== itertools.product child order).
 template <int D>
 __global__ void morton_codes(const double* __restrict__ pts, int64_t n, int Lmax, BinParams bp,
@@ -205,7 +205,7 @@ struct AdmParams {
   double wl, hw, diam, eta;
 };
 
-// geometry.py:210 boxes_admissible with the reference's roundings
+// geometry.py:147 boxes_admissible with the reference's roundings
 template <int D>
 __device__ __forceinline__ bool admissible_cells(const long long* ma, const long long* mb, const AdmParams& ap) {
   double dot = 0.0;
@@ -313,7 +313,7 @@ void build_tree_impl(DevTree& T, const double* Pd, const double* Qd, cudaStream_
   const int d = D;
   Cub cub_;
   const int64_t np = T.np, nq = T.nq;
-  // ---------------- root box (geometry.py:306-310) ----------------
+  // ---------------- root box (geometry.py:243-247) ----------------
   {
     int nb = 512;
     DBuf<double> lo, hi;
@@ -346,7 +346,7 @@ void build_tree_impl(DevTree& T, const double* Pd, const double* Qd, cudaStream_
   }
   // ---------------- Morton codes ----------------
   // deepest level the reference can address before np.ravel_multi_index
-  // overflows (geometry.py:366) or the width underflow stop (geometry.py:332)
+  // overflows (geometry.py:303) or the width underflow stop (geometry.py:269)
   int Lcap = std::min(50, 62 / d);
   T.Lmax = Lcap;
   BinParams bp;
@@ -371,7 +371,7 @@ void build_tree_impl(DevTree& T, const double* Pd, const double* Qd, cudaStream_
     CK(cub::DeviceRadixSort::SortPairs(cub_.tmp.get(), bytes, code_raw[set].get(), code_sorted[set].get(),
                                        idx_raw[set].get(), idx_sorted[set].get(), n, 0, d * Lcap, s));
   }
-  // ---------------- depth (geometry.py:325-377 loop control) ----------------
+  // ---------------- depth (geometry.py:262-314 loop control) ----------------
   DBuf<unsigned long long> runbuf;
   runbuf.alloc(1);
   auto worst_at = [&](int level) -> int64_t {
@@ -620,7 +620,7 @@ void build_tree_impl(DevTree& T, const double* Pd, const double* Qd, cudaStream_
 
 std::unique_ptr<DevTree> build_tree(const double* P, int64_t np, const double* Q, int64_t nq, int d, int shared,
                                     int64_t nu, double eta, bool on_device, cudaStream_t s) {
-  // geometry.py:298-303 argument checks
+  // geometry.py:235-240 argument checks
   if (np == 0 || nq == 0) throw std::invalid_argument("empty point set");
   if (nu < 1) throw std::invalid_argument("invalid leaf capacity");
   if (!(eta > 0)) throw std::invalid_argument("eta must be positive");

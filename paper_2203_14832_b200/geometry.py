@@ -2,7 +2,7 @@
 
 Same public surface as h2cross/geometry.py (PointCloud, Cell, HierTree,
 admissible, build_tree, compute_lists).  ``build_tree`` runs entirely on the
-GPU (libh2b200.so h2b_tree_build, replacing geometry.py:293): Morton codes
+GPU (libh2b200.so h2b_tree_build, replacing geometry.py:230): Morton codes
 from the reference's exact bin recurrence, one radix sort, per-level cells,
 and CSR neighbour / interaction lists.  The returned ``HierTree`` keeps the
 device tree and materialises the reference's Python view (``levels`` dicts of
@@ -21,8 +21,8 @@ import numpy as np
 
 from . import _lib
 
-FULL_GRID_CELL_CAP = 1 << 21  # geometry.py:96
-WIDTH_UNDERFLOW = 2.0**-50  # geometry.py:99
+FULL_GRID_CELL_CAP = 1 << 21  # geometry.py:33
+WIDTH_UNDERFLOW = 2.0**-50  # geometry.py:36
 
 
 @dataclass
@@ -81,7 +81,7 @@ _EMPTY_IDX = np.empty(0, dtype=np.int64)
 
 
 class Cell:
-    """One box of the tree (geometry.py:159)."""
+    """One box of the tree (geometry.py:96)."""
 
     __slots__ = ("level", "multi_index", "center", "half_width", "parent", "children", "t_idx", "s_idx",
                  "neighbors", "interaction_list", "is_leaf", "over_capacity", "_ref_index")
@@ -121,7 +121,7 @@ class Cell:
 
 
 def boxes_admissible(center_x, hw_x, center_y, hw_y, eta: float) -> bool:
-    """Closed-form admissibility for two axis-aligned hypercubes (geometry.py:210)."""
+    """Closed-form admissibility for two axis-aligned hypercubes (geometry.py:147)."""
     d = len(center_x)
     diam = 2.0 * max(hw_x, hw_y) * math.sqrt(d)
     gap = np.maximum(np.abs(np.asarray(center_x) - np.asarray(center_y)) - (hw_x + hw_y), 0.0)
@@ -223,7 +223,7 @@ class HierTree:
         return self._over
 
     def stats_report(self) -> str:
-        """Plain-text summary: depth, cells per level, leaf occupancy histogram (geometry.py:252)."""
+        """Plain-text summary: depth, cells per level, leaf occupancy histogram (geometry.py:189)."""
         out = io.StringIO()
         cloud = self.cloud
         d = cloud.dim
@@ -270,7 +270,7 @@ def _materialize(tree: HierTree):
 
     Nonempty cells, their point sets and parent/child links come from the
     engine.  Empty cells are created where the reference creates them
-    (geometry.py:347-363: the full grid while it has at most
+    (geometry.py:284-300: the full grid while it has at most
     FULL_GRID_CELL_CAP cells, else the children of nonempty cells and of
     their neighbours); their lists are computed here by the reference rule.
     """
@@ -328,7 +328,7 @@ def _materialize(tree: HierTree):
 
 
 def _annotate(levels, level, eta):
-    """geometry.py:385 _annotate_level on the materialised view."""
+    """geometry.py:322 _annotate_level on the materialised view."""
     for cell in levels[level].values():
         parent = cell.parent
         candidates = [ch for nb in parent.neighbors for ch in nb.children]
@@ -345,7 +345,7 @@ def _annotate(levels, level, eta):
 
 
 def build_tree(cloud: PointCloud, nu: int, eta: float) -> HierTree:
-    """Build the uniform 2^d tree and its lists on the GPU (geometry.py:293).
+    """Build the uniform 2^d tree and its lists on the GPU (geometry.py:230).
 
     Raises ValueError for an empty cloud, ``nu`` < 1, or ``eta`` <= 0.
     """
@@ -367,7 +367,7 @@ def build_tree(cloud: PointCloud, nu: int, eta: float) -> HierTree:
 
 
 def compute_lists(tree: HierTree) -> HierTree:
-    """(Re)compute neighbor and interaction lists at every level >= 1 (geometry.py:402).
+    """(Re)compute neighbor and interaction lists at every level >= 1 (geometry.py:339).
 
     The engine computes the lists during ``build_tree``; on the Python view
     this re-derives them from the cell geometry, as the reference does.

@@ -70,6 +70,20 @@ struct DevH2Level {
   const int64_t* n_outd() const { return n_out.n ? n_out.get() : m_in.get(); }
 };
 
+// Compact transfer operators of one level and side (transfer.cuh): the interpolators without their identity
+// (pivot) rows.
+struct CompactOps {
+  DBuf<int> piv_pos;      // per pivot: row position of its identity row in the level's row space, -1 = dense cell
+  DBuf<int64_t> g_ptr;    // n + 1: general-row prefix per cell
+  DBuf<int> g_pos;        // per general row: its row position
+  DBuf<int> g_owner;      // per general row: its cell
+  DBuf<int64_t> op_off;   // n + 1: offset of the cell's g x k block
+  DBuf<double> op_dn;     // [s * g + j] (downward: thread per general row)
+  DBuf<double> op_up;     // [j * k + s] (upward: thread per pivot)
+  int64_t g_total = 0, op_total = 0;
+  int sg_up = 1, sg_dn = 1;  // lanes per output row
+};
+
 // Packed source records of every interaction source list for one RHS width
 // (interact.cuh SrcRec): per level the outgoing pivots, then the leaf points.
 struct RecSet {
@@ -98,9 +112,7 @@ struct DevH2 {
   DBuf<int> item_desc;      // per work item {first target, targets, list begin, list end} (int4)
   DBuf<unsigned char> tabs; // per-list pointer tables for the interaction kernel
   std::vector<DBuf<int>> own_in, own_out;  // per level: pivot position -> owning cell
-  DBuf<int> own_t;                          // sorted target position -> leaf cell
-  std::vector<DBuf<double>> qmat_t;         // per level: transposed column interpolators (upward pass)
-  std::vector<int> up_sg;                   // per level: lanes per output row in the upward pass
+  std::vector<CompactOps> c_in, c_out;      // per level: compact row / column interpolators (c_out empty when symmetric)
   std::vector<DBuf<int>> m_sb, m_end, m_cnt;       // per interaction list: member tables (interact.cuh LevelTab)
   RecSet pack1, pack16;                     // source records for RHS chunks of width 1 / 16
   DBuf<unsigned long long> work_counter;    // persistent interaction kernel: next work item

@@ -6,8 +6,8 @@
 // registers inside one interaction kernel, because on B200 evaluating 1/r in
 // FP64 (~12 FP64 instructions / entry) is ~3x cheaper than streaming the
 // stored 8-byte entry from HBM.  Transfer operators (P2M/M2M/L2L/L2P) are
-// stored dense, column-major, and applied as batched small GEMVs whose
-// operands are contiguous slices thanks to the Morton cell order.
+// applied from compact copies without their identity rows (transfer.cuh) as
+// batched small GEMVs; the Morton cell order keeps every operand contiguous.
 #include <cub/cub.cuh>
 
 #include <cmath>
@@ -15,6 +15,7 @@
 #include <cstring>
 
 #include "interact_sym.cuh"
+#include "transfer.cuh"
 
 namespace h2b {
 
@@ -31,279 +32,6 @@ __global__ void gather_rows(const double* __restrict__ w, const int64_t* __restr
   const double v = w[perm[p] * R + r];
   out[i] = v;
   if (recq) recq[i * rs] = v;  // one RHS: also the charge slot of the source record (no separate pack pass)
-}
-
-// ---- transfer passes as one thread per output row (owner maps give the cell) ----
-__global__ void fill_owner(int64_t ncell, const int64_t* __restrict__ ptr, int* __restrict__ owner) {
-  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c >= ncell) return;
-  for (int64_t p = ptr[c]; p < ptr[c + 1]; p++) owner[p] = (int)c;
-}
-
-// AT_c[j * k + s] = A_c[s * nr + j]: the upward pass reads the column
-// interpolator row-wise, so it gets a transposed copy (coalesced over s)
-__global__ void transpose_cells(int64_t ncell, const int64_t* __restrict__ nrow, const int64_t* __restrict__ kcol,
-                                const double* __restrict__ A, const int64_t* __restrict__ a_off,
-                                double* __restrict__ AT) {
-  const int64_t c = blockIdx.x;
-  if (c >= ncell) return;
-  const int64_t nr = nrow[c], k = kcol[c];
-  const double* Ac = A + a_off[c];
-  double* ATc = AT + a_off[c];
-  for (int64_t q = threadIdx.x; q < nr * k; q += blockDim.x) {
-    const int64_t j = q / k, sidx = q - j * k;
-    ATc[q] = Ac[sidx * nr + j];
-  }
-}
-
-// upward (P2M / M2M): y[p] = sum_j AT_c[j * k + s] x_c[j],  p = out_ptr[c] + s.
-// RB consecutive doubles of a right-hand-side row.  H2B_VEC16: 16-byte loads when the row start is even
-// (R even and r0 even: every RHS row offset is then a multiple of 2 doubles), else scalar loads guarded by R.
-// multi-RHS (R >= 8) transfer passes: lanes per row (upward) and RHS block widths.  Measured at c4
-// (16 RHS; tools/variants.py + time_variants.py): one thread per row x 8 RHS beats 4 lanes x 16 RHS
-// (upward 10.5 -> 5.8 ms: 86 -> fewer registers, 15 -> 2x the resident warps of a latency-bound pass),
-// 8-wide blocks beat 16 for L2L / L2P (3.71 -> 3.18, 2.52 -> 2.08 ms); 4-wide blocks and 8 lanes per
-// row are slower.
-#ifndef H2B_UP_SG
-#define H2B_UP_SG 1
-#endif
-#ifndef H2B_UP_RB
-#define H2B_UP_RB 8
-#endif
-#ifndef H2B_DN_RB
-#define H2B_DN_RB 8
-#endif
-#ifndef H2B_L2P_RB
-#define H2B_L2P_RB 8
-#endif
-#ifndef H2B_VEC16
-#define H2B_VEC16 1
-#endif
-template <int RB>
-__device__ __forceinline__ void load_rhs(const double* __restrict__ p, bool vec, int64_t r0, int64_t R, double (&v)[RB]) {
-  if (H2B_VEC16 && RB % 2 == 0 && vec) {
-    const double2* p2 = reinterpret_cast<const double2*>(p);
-#pragma unroll
-    for (int i = 0; i < RB / 2; i++) {
-      const double2 t = p2[i];
-      v[2 * i] = t.x;
-      v[2 * i + 1] = t.y;
-    }
-  } else {
-#pragma unroll
-    for (int r = 0; r < RB; r++) v[r] = (RB == 1 || r0 + r < R) ? p[r] : 0.0;
-  }
-}
-
-// SG lanes share one output row (j split across them, shuffle-reduced): the
-// upper levels have few rows but long sums (nr ~ 100-200), which one thread
-// per row turns into a long dependent load chain.
-template <int SG, int RB>
-__global__ void up_rows(int64_t nout, const int* __restrict__ owner, const int64_t* __restrict__ out_ptr,
-                        const int64_t* __restrict__ nrow, const double* __restrict__ A,
-                        const int64_t* __restrict__ a_off, const double* __restrict__ x,
-                        const int64_t* __restrict__ x_ptr, const int64_t* __restrict__ x_map,
-                        double* __restrict__ y, int64_t R) {
-  // thread = (output row p, block of RB right-hand sides, lane sub of SG): each operator entry read once
-  // feeds RB accumulators (multi-RHS products are small dense contractions)
-  const int64_t nrb = (R + RB - 1) / RB;
-  const int64_t qq = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t q = qq / SG;
-  const int sub = (int)(qq % SG);
-  const bool ok = q < nout * nrb;
-  double acc[RB];
-#pragma unroll
-  for (int r = 0; r < RB; r++) acc[r] = 0.0;
-  int64_t p = 0, r0 = 0;
-  if (ok) {
-    p = q / nrb;
-    r0 = (q - p * nrb) * RB;
-    const int c = owner[p];
-    const int64_t sidx = p - out_ptr[c], nr = nrow[c], k = out_ptr[c + 1] - out_ptr[c];
-    const double* As = A + a_off[c] + sidx;
-    const double* xc = x + (x_map ? x_ptr[x_map[c]] : x_ptr[c]) * R + r0;
-    const bool vec = (R % 2 == 0) && r0 + RB <= R;
-    for (int64_t j = sub; j < nr; j += SG) {
-      const double a = As[j * k];
-      double xv[RB];
-      load_rhs<RB>(xc + j * R, vec, r0, R, xv);
-#pragma unroll
-      for (int r = 0; r < RB; r++) acc[r] = fma(a, xv[r], acc[r]);
-    }
-  }
-  if constexpr (SG > 1) {
-#pragma unroll
-    for (int r = 0; r < RB; r++)
-#pragma unroll
-      for (int o = SG / 2; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
-  }
-  if (ok && sub == 0)
-#pragma unroll
-    for (int r = 0; r < RB; r++)
-      if (RB == 1 || r0 + r < R) y[p * R + r0 + r] = acc[r];
-}
-
-// Unroll of the P2M/M2M and L2P row loops (measured at the headline: no unrolling beats the compiler's
-// default and unroll 4 / 8 -- upward 0.287 -> 0.267 ms, L2P 0.074 -> 0.066 ms; the L2L loop keeps the default).
-#ifndef H2B_XU
-#define H2B_XU 1
-#endif
-#define H2B_PRAGMA_(x) _Pragma(#x)
-#define H2B_UNROLL_XU(n) H2B_PRAGMA_(unroll n)
-
-// one-RHS-block form (R < 8): SG lanes per output row
-template <int SG>
-__global__ void up_rows1(int64_t nout, const int* __restrict__ owner, const int64_t* __restrict__ out_ptr,
-                         const int64_t* __restrict__ nrow, const double* __restrict__ A,
-                         const int64_t* __restrict__ a_off, const double* __restrict__ x,
-                         const int64_t* __restrict__ x_ptr, const int64_t* __restrict__ x_map,
-                         double* __restrict__ y, int64_t R, double* __restrict__ recq, int rs) {
-  const int64_t qq = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t q = qq / SG;
-  const int sub = (int)(qq % SG);
-  const bool ok = q < nout * R;
-  double acc = 0.0;
-  if (ok) {
-    const int64_t p = q / R, r = q - p * R;
-    const int c = owner[p];
-    const int64_t sidx = p - out_ptr[c], nr = nrow[c], k = out_ptr[c + 1] - out_ptr[c];
-    const double* As = A + a_off[c] + sidx;
-    const double* xc = x + (x_map ? x_ptr[x_map[c]] : x_ptr[c]) * R + r;
-    H2B_UNROLL_XU(H2B_XU)
-    for (int64_t j = sub; j < nr; j += SG) acc = fma(As[j * k], xc[j * R], acc);
-  }
-  if constexpr (SG > 1) {
-#pragma unroll
-    for (int o = SG / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  }
-  if (ok && sub == 0) {
-    y[q] = acc;
-    if (recq) recq[q * rs] = acc;
-  }
-}
-
-void launch_up(int sg, int64_t nout, const int* owner, const int64_t* out_ptr, const int64_t* nrow, const double* A,
-               const int64_t* a_off, const double* x, const int64_t* x_ptr, const int64_t* x_map, double* y,
-               int64_t R, cudaStream_t s, double* recq = nullptr, int rs = 0) {
-  if (R >= 8) {  // register-blocked over H2B_UP_RB right-hand sides, H2B_UP_SG lanes per row
-    const int64_t thr = std::max<int64_t>(nout * ((R + H2B_UP_RB - 1) / H2B_UP_RB), 1) * H2B_UP_SG;
-    up_rows<H2B_UP_SG, H2B_UP_RB><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R);
-    CKL();
-    return;
-  }
-  const int64_t thr = std::max<int64_t>(nout * R, 1) * sg;
-  switch (sg) {
-    case 1: up_rows1<1><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R, recq, rs); break;
-    case 2: up_rows1<2><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R, recq, rs); break;
-    case 4: up_rows1<4><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R, recq, rs); break;
-    case 8: up_rows1<8><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R, recq, rs); break;
-    default: up_rows1<16><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, nrow, A, a_off, x, x_ptr, x_map, y, R, recq, rs); break;
-  }
-  CKL();
-}
-
-// lanes per row for a level: enough rows in flight, short per-lane chains
-int up_group(int64_t rows, int64_t nr_avg) {
-  int sg = 1;
-  while (sg < 16 && (nr_avg / sg > 24 || rows * sg < 148 * 1024)) {
-    if (nr_avg / (2 * sg) < 4) break;
-    sg *= 2;
-  }
-  return sg;
-}
-
-// downward (L2L): rows of the children stacked under parent P: u_child[q] += sum_s P_P[s * nr + i] u_P[s]
-// (thread = child row x block of RB right-hand sides)
-template <int RB>
-__global__ void down_rows(int64_t nin_child, const int* __restrict__ child_owner, const int64_t* __restrict__ parent,
-                          const int64_t* __restrict__ ch_ptr, const int64_t* __restrict__ in_ptr_child,
-                          const int64_t* __restrict__ in_ptr, const int64_t* __restrict__ kin,
-                          const int64_t* __restrict__ nrow, const double* __restrict__ Pm,
-                          const int64_t* __restrict__ pm_off, const double* __restrict__ uin,
-                          double* __restrict__ uin_child, int64_t R) {
-  const int64_t nrb = (R + RB - 1) / RB;
-  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q >= nin_child * nrb) return;
-  const int64_t p = q / nrb, r0 = (q - p * nrb) * RB;
-  const int64_t P = parent[child_owner[p]];
-  const int64_t i = p - in_ptr_child[ch_ptr[P]], nr = nrow[P], k = kin[P];
-  const double* Pc = Pm + pm_off[P] + i;
-  const double* uc = uin + in_ptr[P] * R + r0;
-  double acc[RB];
-#pragma unroll
-  for (int r = 0; r < RB; r++) acc[r] = 0.0;
-  const bool vec = (R % 2 == 0) && r0 + RB <= R;
-  for (int64_t t = 0; t < k; t++) {
-    const double a = Pc[t * nr];
-    double uv[RB];
-    load_rhs<RB>(uc + t * R, vec, r0, R, uv);
-#pragma unroll
-    for (int r = 0; r < RB; r++) acc[r] = fma(a, uv[r], acc[r]);
-  }
-#pragma unroll
-  for (int r = 0; r < RB; r++)
-    if (RB == 1 || r0 + r < R) uin_child[p * R + r0 + r] += acc[r];
-}
-
-// one-RHS form for the upper levels (few child rows, long parent ranks): SG lanes per child row split the
-// parent's k columns, shuffle-reduced (a latency-bound 10-20 us launch otherwise)
-template <int SG>
-__global__ void down_rows_sg(int64_t nin_child, const int* __restrict__ child_owner, const int64_t* __restrict__ parent,
-                             const int64_t* __restrict__ ch_ptr, const int64_t* __restrict__ in_ptr_child,
-                             const int64_t* __restrict__ in_ptr, const int64_t* __restrict__ kin,
-                             const int64_t* __restrict__ nrow, const double* __restrict__ Pm,
-                             const int64_t* __restrict__ pm_off, const double* __restrict__ uin,
-                             double* __restrict__ uin_child, int64_t R) {
-  const int64_t qq = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t q = qq / SG;
-  const int sub = (int)(qq % SG);
-  const bool ok = q < nin_child * R;
-  double acc = 0.0;
-  if (ok) {
-    const int64_t p = q / R, r = q - p * R;
-    const int64_t P = parent[child_owner[p]];
-    const int64_t i = p - in_ptr_child[ch_ptr[P]], nr = nrow[P], k = kin[P];
-    const double* Pc = Pm + pm_off[P] + i;
-    const double* uc = uin + in_ptr[P] * R + r;
-    for (int64_t t = sub; t < k; t += SG) acc = fma(Pc[t * nr], uc[t * R], acc);
-  }
-#pragma unroll
-  for (int o = SG / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (ok && sub == 0) uin_child[q] += acc;
-}
-
-// leaves: u[perm[p]] = near[p] + sum_s P_c[s * m + a] u_in(c)[s]  (thread = point x block of RB RHS)
-template <int RB>
-__global__ void l2p_rows(int64_t np, const int* __restrict__ owner, const int64_t* __restrict__ t_ptr,
-                         const double* __restrict__ pm, const int64_t* __restrict__ pm_off,
-                         const int64_t* __restrict__ kin, const int64_t* __restrict__ in_ptr,
-                         const double* __restrict__ uin, const double* __restrict__ near,
-                         const int64_t* __restrict__ perm, double* __restrict__ u, int64_t R) {
-  const int64_t nrb = (R + RB - 1) / RB;
-  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q >= np * nrb) return;
-  const int64_t p = q / nrb, r0 = (q - p * nrb) * RB;
-  const bool vec = (R % 2 == 0) && r0 + RB <= R;
-  double v[RB];
-  load_rhs<RB>(near + p * R + r0, vec, r0, R, v);
-  if (pm) {
-    const int c = owner[p];
-    const int64_t a = p - t_ptr[c], m = t_ptr[c + 1] - t_ptr[c], k = kin[c];
-    const double* Pc = pm + pm_off[c] + a;
-    const double* uc = uin + in_ptr[c] * R + r0;
-    H2B_UNROLL_XU(H2B_XU)
-    for (int64_t t = 0; t < k; t++) {
-      const double w = Pc[t * m];
-      double uv[RB];
-      load_rhs<RB>(uc + t * R, vec, r0, R, uv);
-#pragma unroll
-      for (int r = 0; r < RB; r++) v[r] = fma(w, uv[r], v[r]);
-    }
-  }
-  const int64_t dst = perm[p] * R + r0;
-#pragma unroll
-  for (int r = 0; r < RB; r++)
-    if (RB == 1 || r0 + r < R) u[dst + r] = v[r];
 }
 
 void interact_all(int d, int kind, const DevH2& h, int64_t R, int64_t r0, int nr, const KParams& kp,
@@ -734,30 +462,27 @@ void ensure_scratch(DevH2& h, int64_t R, cudaStream_t s) {
         CKL();
       }
     }
-    h.qmat_t.resize(T.depth + 1);
+    // compact transfer operators (transfer.cuh): rows of a cell = its children's stacked pivots, at the leaves
+    // its points
+    h.c_in.clear();
+    h.c_out.clear();
+    h.c_in.resize(T.depth + 1);
+    if (!h.symmetric) h.c_out.resize(T.depth + 1);
     for (int l = 2; l <= T.depth; l++) {
+      const DevLevel& Lv = T.lv[l];
       const DevH2Level& HL = h.lv[l];
-      const size_t nq = h.symmetric ? HL.pmat.n : HL.qmat.n;
-      h.qmat_t[l].alloc(std::max<size_t>(nq, 1), &h.mem);
-      if (HL.n)
-        transpose_cells<<<(unsigned)HL.n, 128, 0, s>>>(HL.n, HL.n_outd(), HL.koutd(), HL.qmatd(), HL.qm_offd(),
-                                                        h.qmat_t[l].get());
-      CKL();
+      const bool leaf = l == T.depth;
+      const int64_t* in_base = leaf ? Lv.t_ptr.get() : h.lv[l + 1].in_ptr.get();
+      const int64_t in_space = leaf ? T.np : h.lv[l + 1].in_total;
+      build_compact(h.c_in[l], HL.n, HL.in_total, HL.in_ptr.get(), HL.m_in.get(), HL.pmat.get(), HL.pm_off.get(),
+                    in_base, leaf ? nullptr : Lv.ch_ptr.get(), in_space, true, h.symmetric != 0, &h.mem, s);
+      if (!h.symmetric) {
+        const int64_t* out_base = leaf ? (T.shared ? Lv.t_ptr.get() : Lv.s_ptr.get()) : h.lv[l + 1].out_ptrd();
+        const int64_t out_space = leaf ? T.nq : h.lv[l + 1].out_total;
+        build_compact(h.c_out[l], HL.n, HL.out_total, HL.out_ptrd(), HL.n_outd(), HL.qmatd(), HL.qm_offd(), out_base,
+                      leaf ? nullptr : Lv.ch_ptr.get(), out_space, false, true, &h.mem, s);
+      }
     }
-    // lanes per output row of the upward pass, per level (from the mean column-interpolator height)
-    h.up_sg.assign(T.depth + 1, 1);
-    for (int l = 2; l <= T.depth; l++) {
-      const DevH2Level& HL = h.lv[l];
-      const int64_t rows = HL.out_total;
-      const int64_t nr_sum = (int64_t)(h.symmetric ? HL.pmat.n : HL.qmat.n);  // sum over cells of nr * k
-      const int64_t nr_avg = rows ? nr_sum / rows : 0;
-      h.up_sg[l] = up_group(rows, nr_avg);
-      while (h.up_sg[l] > 16) h.up_sg[l] /= 2;
-    }
-    const DevLevel& Lf = T.lv[T.depth];
-    h.own_t.alloc(std::max<int64_t>(T.np, 1), &h.mem);
-    fill_owner<<<nblk(Lf.n, 256), 256, 0, s>>>(Lf.n, Lf.t_ptr.get(), h.own_t.get());
-    CKL();
   }
   h.pack1 = RecSet();
   h.pack16 = RecSet();
@@ -833,19 +558,16 @@ void matvec(DevH2& h, const double* w, double* u, int64_t R, cudaStream_t s) {
   if (L >= 2) {
     // ---- upward pass: P2M at the leaves, then M2M (one or a few threads per output row) ----
     auto own_out = [&](int l) { return h.symmetric ? h.own_in[l].get() : h.own_out[l].get(); };
+    auto c_up = [&](int l) -> const CompactOps& { return h.symmetric ? h.c_in[l] : h.c_out[l]; };
     {
-      const DevLevel& Lv = T.lv[L];
       const DevH2Level& HL = h.lv[L];
-      launch_up(h.up_sg[L], HL.out_total, own_out(L), HL.out_ptrd(), HL.n_outd(), h.qmat_t[L].get(), HL.qm_offd(),
-                h.w_sorted.get(), T.shared ? Lv.t_ptr.get() : Lv.s_ptr.get(), nullptr, h.wout[L].get(), R, s,
+      launch_up(c_up(L), HL.out_total, own_out(L), HL.out_ptrd(), h.w_sorted.get(), h.wout[L].get(), R, s,
                 recq(L - 2), rs1);
     }
     for (int l = L - 1; l >= 2; l--) {
-      const DevLevel& Lv = T.lv[l];
       const DevH2Level& HL = h.lv[l];
-      const DevH2Level& HC = h.lv[l + 1];
-      launch_up(h.up_sg[l], HL.out_total, own_out(l), HL.out_ptrd(), HL.n_outd(), h.qmat_t[l].get(), HL.qm_offd(),
-                h.wout[l + 1].get(), HC.out_ptrd(), Lv.ch_ptr.get(), h.wout[l].get(), R, s, recq(l - 2), rs1);
+      launch_up(c_up(l), HL.out_total, own_out(l), HL.out_ptrd(), h.wout[l + 1].get(), h.wout[l].get(), R, s,
+                recq(l - 2), rs1);
     }
   }
   if (g_profile) CK(cudaEventRecord(ev[1], s));
@@ -863,58 +585,18 @@ void matvec(DevH2& h, const double* w, double* u, int64_t R, cudaStream_t s) {
     else interact_all(d, h.kind, h, R, ch.first, ch.second, kp, s);
   }
   if (g_profile) CK(cudaEventRecord(ev[2], s));
-  // ---- downward pass (L2L), one thread per child row ----
-  for (int l = 2; l < L; l++) {
-    const DevLevel& Lv = T.lv[l];
-    const DevLevel& Lc = T.lv[l + 1];
-    const DevH2Level& HL = h.lv[l];
-    const DevH2Level& HC = h.lv[l + 1];
-    if (R >= 8)
-      down_rows<H2B_DN_RB><<<nblk(HC.in_total * ((R + H2B_DN_RB - 1) / H2B_DN_RB), 256), 256, 0, s>>>(
-          HC.in_total, h.own_in[l + 1].get(), Lc.parent.get(), Lv.ch_ptr.get(), HC.in_ptr.get(), HL.in_ptr.get(),
-          HL.kin.get(), HL.m_in.get(), HL.pmat.get(), HL.pm_off.get(), h.uin[l].get(), h.uin[l + 1].get(), R);
-    else {
-      // large levels keep one thread per row (measured); small ones split the parent's columns over lanes
-      const int sg = HC.in_total * R < 148 * 1024 ? up_group(HC.in_total * R, HL.in_total / std::max<int64_t>(HL.n, 1)) : 1;
-      const int64_t thr = std::max<int64_t>(HC.in_total * R, 1) * sg;
-#define H2B_DOWN_SG(G)                                                                                          \
-  down_rows_sg<G><<<nblk(thr, 256), 256, 0, s>>>(HC.in_total, h.own_in[l + 1].get(), Lc.parent.get(),           \
-                                                 Lv.ch_ptr.get(), HC.in_ptr.get(), HL.in_ptr.get(), HL.kin.get(), \
-                                                 HL.m_in.get(), HL.pmat.get(), HL.pm_off.get(), h.uin[l].get(),  \
-                                                 h.uin[l + 1].get(), R)
-      if (sg == 1) {
-        down_rows<1><<<nblk(HC.in_total * R, 256), 256, 0, s>>>(
-            HC.in_total, h.own_in[l + 1].get(), Lc.parent.get(), Lv.ch_ptr.get(), HC.in_ptr.get(), HL.in_ptr.get(),
-            HL.kin.get(), HL.m_in.get(), HL.pmat.get(), HL.pm_off.get(), h.uin[l].get(), h.uin[l + 1].get(), R);
-      } else if (sg == 2) {
-        H2B_DOWN_SG(2);
-      } else if (sg == 4) {
-        H2B_DOWN_SG(4);
-      } else if (sg == 8) {
-        H2B_DOWN_SG(8);
-      } else {
-        H2B_DOWN_SG(16);
-      }
-#undef H2B_DOWN_SG
-    }
-    CKL();
-  }
+  // ---- downward pass (L2L): one thread (upper levels: a few lanes) per general child row, one per pivot ----
+  for (int l = 2; l < L; l++)
+    launch_down<false>(h.c_in[l], h.lv[l].in_total, h.lv[l].in_ptr.get(), h.uin[l].get(), h.uin[l + 1].get(), nullptr,
+                       nullptr, R, s);
   if (g_profile) CK(cudaEventRecord(ev[3], s));
-  // ---- L2P + near field, scattered to the caller's order (one thread per target) ----
-  {
-    const DevLevel& Lv = T.lv[L];
-    const bool far = L >= 2;
-    const DevH2Level* HL = far ? &h.lv[L] : nullptr;
-    auto l2p = [&](auto kern, int64_t nthreads) {
-      kern<<<nblk(nthreads, 256), 256, 0, s>>>(T.np, h.own_t.get(), Lv.t_ptr.get(), far ? HL->pmat.get() : nullptr,
-                                               far ? HL->pm_off.get() : nullptr, far ? HL->kin.get() : nullptr,
-                                               far ? HL->in_ptr.get() : nullptr, far ? h.uin[L].get() : nullptr,
-                                               h.near.get(), T.t_perm.get(), u, R);
-    };
-    if (R >= 8) l2p(l2p_rows<H2B_L2P_RB>, T.np * ((R + H2B_L2P_RB - 1) / H2B_L2P_RB));
-    else l2p(l2p_rows<1>, T.np * R);
-    CKL();
-  }
+  // ---- L2P + near field, scattered to the caller's order ----
+  if (L >= 2)
+    launch_down<true>(h.c_in[L], h.lv[L].in_total, h.lv[L].in_ptr.get(), h.uin[L].get(), u, h.near.get(),
+                      T.t_perm.get(), R, s);
+  else
+    scatter_near<<<nblk(T.np * R, 256), 256, 0, s>>>(T.np, h.near.get(), T.t_perm.get(), u, R);
+  CKL();
   if (g_profile) {
     CK(cudaEventRecord(ev[4], s));
     CK(cudaEventSynchronize(ev[4]));

@@ -358,16 +358,21 @@ def run_b200(args, cfg, world, rank, local):
     # transfer passes: algorithmic bytes = the interpolation operators read once per product (P2M / M2M read
     # the column interpolators, L2L / L2P the row interpolators; pmat per level = sum over cells of rows x k) plus
     # the coefficient vectors they stream (w in, pivot coefficients written and read, u out), nrhs columns each
-    op_bytes = 0
+    op_bytes = dense_op_bytes = idx_bytes = 0
     vec_bytes = 8 * nrhs * (2 * n)  # w_sorted read + u written (near-field partials read by L2P: + n)
     vec_bytes += 8 * nrhs * n
     for lev in range(2, depth + 1):
         m_in, k_in = h2.array(lev, "m_in"), h2.array(lev, "k_in")
         n_out, k_out = h2.array(lev, "n_out"), h2.array(lev, "k_out")
-        op_bytes += 8 * int(np.dot(m_in, k_in)) + 8 * int(np.dot(n_out, k_out))
+        # compact operators (csrc/transfer.cuh): the k identity rows of every interpolator are not stored
+        op_bytes += 8 * int(np.dot(m_in - k_in, k_in)) + 8 * int(np.dot(n_out - k_out, k_out))
+        dense_op_bytes += 8 * int(np.dot(m_in, k_in)) + 8 * int(np.dot(n_out, k_out))
+        # row maps: position (+ owner downward) per general row, identity-row position (+ owner upward) per pivot
+        idx_bytes += 4 * (int((n_out - k_out).sum()) + 2 * int(k_out.sum()))
+        idx_bytes += 4 * (2 * int((m_in - k_in).sum()) + int(k_in.sum()))
         vec_bytes += 8 * nrhs * 4 * int(k_in.sum())  # coefficients: written + read up, read + written down
     tr_ms = stage[0] + stage[2] + stage[3]
-    tr_bytes = op_bytes + vec_bytes
+    tr_bytes = op_bytes + idx_bytes + vec_bytes
     # setup: the ACA's residual sweeps (reference operation order, _core.pyx:70-191): step t re-reads the t previous
     # residual rows / columns of the cell's block (n + m entries each), once for the residual and once for the
     # stopping test's cross products.  nevals per cell ~ k (n + m), so operand bytes ~ 8 (k - 1) nevals and
@@ -387,9 +392,10 @@ def run_b200(args, cfg, world, rank, local):
                   "fp64_probe_tflops": probe, "frac_of_probe": achieved / probe,
                   "flops": flops, "ms": inter_ms, "flops_per_pair": fpp, "evaluated_pairs": evaluated,
                   "applied_entries_per_s": (pairs_m2l + pairs_p2p) / (inter_ms * 1e-3)}
-    roof_tr = {"bound": "hbm", "kernel": "up_rows/down_rows/l2p_rows (P2M, M2M, L2L, L2P)",
+    roof_tr = {"bound": "hbm", "kernel": "up_compact/down_compact (P2M, M2M, L2L, L2P on compact interpolators)",
                "achieved": tr_bytes / (tr_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                "frac": tr_bytes / (tr_ms * 1e-3) / 1e9 / hbm_peak, "bytes": tr_bytes, "operator_bytes": op_bytes,
+               "dense_operator_bytes": dense_op_bytes,
                "ms": tr_ms, "peak_source": hbm_src}
     roof_setup = {"n2_per_s": float(n) ** 2 / setup_s, "ms": setup_s * 1e3,
                   "aca_operand_bytes_model": aca_bytes, "aca_achieved_GBps": aca_bytes / (nnca_ms * 1e-3) / 1e9,

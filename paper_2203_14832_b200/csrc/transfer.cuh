@@ -17,6 +17,9 @@
 #pragma once
 #include <cub/cub.cuh>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "engine.cuh"
 
 namespace h2b {
@@ -183,6 +186,10 @@ inline void build_compact(CompactOps& C, int64_t n, int64_t npiv, const int64_t*
   C.sg_up = lane_group(npiv, g_avg);
   C.sg_dn = C.g_total < 148 * 1024 ? lane_group(C.g_total, k_avg) : 1;
   CK(cudaStreamSynchronize(s));  // the temporaries above are released on return
+  if (getenv("H2B_SETUP_VERBOSE"))
+    fprintf(stderr, "[h2b] compact transfers: %lld cells, %lld pivots, %lld general rows of %lld, %.1f MB per layout, lanes up %d down %d\n",
+            (long long)n, (long long)npiv, (long long)C.g_total, (long long)rowspace, 8e-6 * (double)C.op_total,
+            C.sg_up, C.sg_dn);
 }
 
 // RB consecutive doubles of a right-hand-side row: 16-byte loads when every row start is even

@@ -67,7 +67,11 @@ int64_t h2b_tree_get(const h2b_tree* t, int level, int what, int64_t* dst);
 /* max_rank < 0 means None (cap = min(rows, cols)). */
 int h2b_assemble(const h2b_tree* t, int kind, double a, double eps, int force_general, int64_t max_rank,
                  void* stream, h2b_h2** out);
+/* Both free functions first wait for the last work submitted on the handle (any stream).  Free every H2 built
+ * on a tree before the tree. */
 void h2b_h2_free(h2b_h2* h);
+/* Releases the per-device ACA workspace arenas kept between assemblies (tens of GB after a large setup). */
+int h2b_release_workspace(void);
 /* per level (>= 2), reference cell order.  what: 0 k_in 1 k_out 2 t_in
  * 3 s_in 4 t_out 5 s_out 6 nevals 7 converged(in) 8 m_in(rows of the row
  * interpolator) 9 n_out(rows of the column interpolator) */
@@ -82,7 +86,13 @@ int h2b_h2_stats(const h2b_h2* h, int64_t* stats);
 
 /* ---- matvec: matvec.py:142 h2_matvec ---- */
 /* w: (n_sources, nrhs) row-major, u: (n_targets, nrhs). */
-int h2b_matvec(const h2b_h2* h, const double* w, double* u, int64_t nrhs, int on_device, void* stream);
+/* The product uses scratch owned by h: concurrent callers on one h are serialised (host mutex), and a call on a
+ * stream other than the previous one first waits (cudaStreamWaitEvent) for the previous call's work.  Scratch
+ * sets of up to four right-hand-side widths are kept, so alternating nrhs does not rebuild them. */
+int h2b_matvec(h2b_h2* h, const double* w, double* u, int64_t nrhs, int on_device, void* stream);
+/* Page-locked host memory for w / u of the host-pointer calls (on_device = 0). */
+int h2b_host_alloc(void** p, int64_t bytes);
+void h2b_host_free(void* p);
 /* Number of kernel launches one h2b_matvec call issues (for bench accounting). */
 int64_t h2b_matvec_launches(const h2b_h2* h, int64_t nrhs);
 /* Per-stage device times (ms) of the last profiled matvec: [p2m+m2m, m2l, l2l, p2p+l2p, total];
@@ -96,8 +106,9 @@ int h2b_fp64_peak(double* tflops);
 /* ---- dense oracles: matvec.py:233 dense_matvec / :245 dense_rows ---- */
 int h2b_dense_matvec(int kind, double a, const double* P, int64_t np, const double* Q, int64_t nq, int d,
                      const double* w, double* u, int64_t nrhs, int on_device, void* stream);
-int h2b_dense_rows(int kind, double a, const double* P, const int64_t* rows, int64_t nrows, const double* Q,
-                   int64_t nq, int d, const double* w, double* u);
+/* rows[i] must lie in [0, np) (ValueError otherwise; the reference raises IndexError) */
+int h2b_dense_rows(int kind, double a, const double* P, int64_t np, const int64_t* rows, int64_t nrows,
+                   const double* Q, int64_t nq, int d, const double* w, double* u);
 
 #ifdef __cplusplus
 }

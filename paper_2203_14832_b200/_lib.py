@@ -70,8 +70,12 @@ def _declare(L):
     L.h2b_fp64_peak.argtypes = [_dp]
     L.h2b_dense_matvec.argtypes = [ctypes.c_int, ctypes.c_double, _vp, ctypes.c_int64, _vp, ctypes.c_int64,
                                    ctypes.c_int, _vp, _vp, ctypes.c_int64, ctypes.c_int, _vp]
-    L.h2b_dense_rows.argtypes = [ctypes.c_int, ctypes.c_double, _dp, _i64p, ctypes.c_int64, _dp, ctypes.c_int64,
-                                 ctypes.c_int, _dp, _dp]
+    L.h2b_dense_rows.argtypes = [ctypes.c_int, ctypes.c_double, _dp, ctypes.c_int64, _i64p, ctypes.c_int64, _dp,
+                                 ctypes.c_int64, ctypes.c_int, _dp, _dp]
+    L.h2b_host_alloc.argtypes = [ctypes.POINTER(_vp), ctypes.c_int64]
+    L.h2b_host_free.argtypes = [_vp]
+    L.h2b_host_free.restype = None
+    L.h2b_release_workspace.argtypes = []
     return L
 
 
@@ -91,6 +95,7 @@ EXPORTS = (
     "h2b_tree_free", "h2b_tree_info", "h2b_tree_ncells", "h2b_tree_get", "h2b_assemble", "h2b_h2_free",
     "h2b_h2_get_i64", "h2b_h2_get_interp", "h2b_h2_stats", "h2b_matvec", "h2b_matvec_launches",
     "h2b_set_profiling", "h2b_last_stage_ms", "h2b_fp64_peak", "h2b_dense_matvec", "h2b_dense_rows",
+    "h2b_host_alloc", "h2b_host_free", "h2b_release_workspace",
 )
 
 

@@ -40,16 +40,46 @@ struct LevelHost {
 
 }  // namespace
 
+// Stream discipline.  Every handle carries an event recorded after the last work submitted on its behalf.  A
+// call on a different stream first makes that stream wait for the event (the per-H2 matvec scratch and the
+// tree arrays are then never touched by two streams at once), host callers are serialised by the handle's
+// mutex, and the free functions wait for the event before releasing device memory, so dropping a handle while
+// its last product is still running on a non-blocking stream is safe.
+struct Tail {
+  cudaEvent_t ev = nullptr;
+  cudaStream_t last = nullptr;
+  bool used = false;
+  void enter(cudaStream_t s) {  // order s after the previous call if that ran on another stream
+    if (used && s != last && ev) CK(cudaStreamWaitEvent(s, ev, 0));
+  }
+  void leave(cudaStream_t s) {
+    if (!ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(ev, s));
+    last = s;
+    used = true;
+  }
+  void drain() {  // host-side wait for the last submitted work, then drop the event
+    if (ev) {
+      cudaEventSynchronize(ev);
+      cudaEventDestroy(ev);
+      ev = nullptr;
+    }
+  }
+};
+
 struct h2b_tree {
   std::unique_ptr<DevTree> t;
   std::vector<LevelHost> host;
   std::vector<std::vector<int64_t>> perm, inv;  // per level (host copies)
   std::mutex mu;
+  Tail tail;
 };
 
 struct h2b_h2 {
   std::unique_ptr<DevH2> h;
   h2b_tree* tree;
+  std::mutex mu;
+  Tail tail;
 };
 
 namespace {
@@ -185,6 +215,7 @@ int h2b_tree_build(const double* P, int64_t np, const double* Q, int64_t nq, int
     try {
       StreamScope sc((cudaStream_t)stream);
       T->t = build_tree(P, np, Q, nq, d, shared, nu, eta, on_device != 0, (cudaStream_t)stream);
+      T->tail.leave((cudaStream_t)stream);
     } catch (...) {
       delete T;
       throw;
@@ -193,7 +224,11 @@ int h2b_tree_build(const double* P, int64_t np, const double* Q, int64_t nq, int
   });
 }
 
-void h2b_tree_free(h2b_tree* t) { delete t; }
+void h2b_tree_free(h2b_tree* t) {
+  if (!t) return;
+  t->tail.drain();  // free the H2 matrices built on a tree before the tree itself
+  delete t;
+}
 
 int h2b_tree_info(const h2b_tree* t, int* depth, int* over_capacity, double* mid, double* half) {
   return guarded([&] {
@@ -245,8 +280,16 @@ int h2b_assemble(const h2b_tree* t, int kind, double a, double eps, int force_ge
     auto H = new h2b_h2();
     H->tree = const_cast<h2b_tree*>(t);
     try {
-      StreamScope sc((cudaStream_t)stream);
-      H->h = assemble(*t->t, kind, a, eps, force_general != 0, max_rank, (cudaStream_t)stream);
+      const cudaStream_t s = (cudaStream_t)stream;
+      StreamScope sc(s);
+      {
+        std::lock_guard<std::mutex> g(H->tree->mu);
+        H->tree->tail.enter(s);
+      }
+      H->h = assemble(*t->t, kind, a, eps, force_general != 0, max_rank, s);
+      H->tail.leave(s);
+      std::lock_guard<std::mutex> g(H->tree->mu);
+      H->tree->tail.leave(s);
     } catch (...) {
       delete H;
       throw;
@@ -255,7 +298,15 @@ int h2b_assemble(const h2b_tree* t, int kind, double a, double eps, int force_ge
   });
 }
 
-void h2b_h2_free(h2b_h2* h) { delete h; }
+void h2b_h2_free(h2b_h2* h) {
+  if (!h) return;
+  h->tail.drain();
+  delete h;
+}
+
+int h2b_release_workspace(void) {
+  return guarded([&] { release_workspace(); });
+}
 
 int64_t h2b_h2_get_i64(const h2b_h2* hc, int level, int what, int64_t* dst) {
   int64_t ret = 0;
@@ -353,15 +404,19 @@ int h2b_h2_stats(const h2b_h2* hc, int64_t* st) {
   });
 }
 
-int h2b_matvec(const h2b_h2* hc, const double* w, double* u, int64_t nrhs, int on_device, void* stream) {
+int h2b_matvec(h2b_h2* hc, const double* w, double* u, int64_t nrhs, int on_device, void* stream) {
   return guarded([&] {
     DevH2& h = *hc->h;
     const DevTree& T = *h.t;
     if (nrhs < 1) throw std::invalid_argument("nrhs must be positive");
     cudaStream_t s = (cudaStream_t)stream;
     StreamScope sc(s);
+    // the product writes per-H2 scratch: one caller at a time, and a new stream waits for the previous one
+    std::lock_guard<std::mutex> g(hc->mu);
+    hc->tail.enter(s);
     if (on_device) {
       matvec(h, w, u, nrhs, s);
+      hc->tail.leave(s);
       return;
     }
     if ((int64_t)h.io_w.n < T.nq * nrhs) h.io_w.alloc(T.nq * nrhs);
@@ -369,8 +424,20 @@ int h2b_matvec(const h2b_h2* hc, const double* w, double* u, int64_t nrhs, int o
     CK(cudaMemcpyAsync(h.io_w.get(), w, T.nq * nrhs * 8, cudaMemcpyHostToDevice, s));
     matvec(h, h.io_w.get(), h.io_u.get(), nrhs, s);
     CK(cudaMemcpyAsync(u, h.io_u.get(), T.np * nrhs * 8, cudaMemcpyDeviceToHost, s));
+    hc->tail.leave(s);
     CK(cudaStreamSynchronize(s));
   });
+}
+
+/* page-locked host buffers for the host-pointer calls (copies from pinned memory run at the full PCIe rate) */
+int h2b_host_alloc(void** p, int64_t bytes) {
+  return guarded([&] {
+    if (bytes < 0) throw std::invalid_argument("negative size");
+    CK(cudaHostAlloc(p, (size_t)std::max<int64_t>(bytes, 1), cudaHostAllocDefault));
+  });
+}
+void h2b_host_free(void* p) {
+  if (p) cudaFreeHost(p);
 }
 
 int64_t h2b_matvec_launches(const h2b_h2* h, int64_t nrhs) { return matvec_launches(*h->h, nrhs); }
@@ -413,13 +480,13 @@ int h2b_dense_matvec(int kind, double a, const double* P, int64_t np, const doub
   });
 }
 
-int h2b_dense_rows(int kind, double a, const double* P, const int64_t* rows, int64_t nrows, const double* Q,
-                   int64_t nq, int d, const double* w, double* u) {
+int h2b_dense_rows(int kind, double a, const double* P, int64_t np, const int64_t* rows, int64_t nrows,
+                   const double* Q, int64_t nq, int d, const double* w, double* u) {
   return guarded([&] {
     if (!kind_valid(kind)) throw std::invalid_argument("unknown kernel kind");
     if (nrows == 0) return;
-    int64_t np = 0;
-    for (int64_t i = 0; i < nrows; i++) np = std::max(np, rows[i] + 1);
+    for (int64_t i = 0; i < nrows; i++)
+      if (rows[i] < 0 || rows[i] >= np) throw std::invalid_argument("row index out of range");
     DBuf<double> dp, dq, dw, du;
     DBuf<int64_t> dr;
     dp.alloc(np * d);

@@ -93,7 +93,20 @@ struct RecSet {
   int64_t total = 0;
 };
 
-struct DevH2 {
+// Matvec scratch of one right-hand-side width: everything whose size or device pointers depend on nrhs.  The
+// active set lives in DevH2 (base class); sets of other widths are parked in DevH2::parked, so alternating
+// widths (e.g. a 16-RHS block product between single-vector products) does not rebuild the source records.
+struct MatvecScratch {
+  int64_t scratch_nrhs = 0;
+  DBuf<double> w_sorted;
+  std::vector<DBuf<double>> wout, uin;
+  DBuf<double> near;        // near-field sums (sorted target order)
+  DBuf<unsigned char> tabs; // per-list pointer tables for the interaction kernel
+  RecSet pack1, pack16;     // source records for RHS chunks of width 1 / 16
+  DBuf<unsigned char> sym_tabs;
+};
+
+struct DevH2 : MatvecScratch {
   const DevTree* t = nullptr;
   int kind = 0, symmetric = 1;
   double a = 0, eps = 0;
@@ -101,20 +114,15 @@ struct DevH2 {
   std::vector<DevH2Level> lv;  // indexed by level; levels < 2 empty
   int64_t evals_pivots = 0, evals_couplings = 0, evals_nearfield = 0, max_rank = 0, cells_visited = 0;
   int64_t setup_ns = 0, unconverged = 0;
-  // matvec scratch (allocated lazily, sized for nrhs)
-  int64_t scratch_nrhs = 0;
-  DBuf<double> w_sorted, u_tmp;
-  std::vector<DBuf<double>> wout, uin;
+  // matvec scratch of other RHS widths (most recently used last; at most 3 parked)
+  std::vector<MatvecScratch> parked;
   DBuf<double> io_w, io_u;  // device staging for host-pointer calls
-  DBuf<double> near;        // near-field sums (sorted target order)
   DBuf<int64_t> items;      // interaction work list ((list << 40) | cell), by descending pair count
   int64_t n_items = 0;
   DBuf<int> item_desc;      // per work item {first target, targets, list begin, list end} (int4)
-  DBuf<unsigned char> tabs; // per-list pointer tables for the interaction kernel
   std::vector<DBuf<int>> own_in, own_out;  // per level: pivot position -> owning cell
   std::vector<CompactOps> c_in, c_out;      // per level: compact row / column interpolators (c_out empty when symmetric)
   std::vector<DBuf<int>> m_sb, m_end, m_cnt;       // per interaction list: member tables (interact.cuh LevelTab)
-  RecSet pack1, pack16;                     // source records for RHS chunks of width 1 / 16
   DBuf<unsigned long long> work_counter;    // persistent interaction kernel: next work item
   // symmetric one-RHS interaction kernel (interact_sym.cuh): upper member tables per list (partners Y > X),
   // work items (list, cell) by descending pair count, descriptors and per-list tables
@@ -123,7 +131,6 @@ struct DevH2 {
   DBuf<int> sym_desc;
   int64_t n_sym_items = 0;
   bool sym_wide = false;  // 32-target chunks (most pairs in items with > 16 targets) instead of 16
-  DBuf<unsigned char> sym_tabs;
   bool sym_ready = false;
 };
 
@@ -133,6 +140,7 @@ std::unique_ptr<DevTree> build_tree(const double* P, int64_t np, const double* Q
 // nnca.cu
 std::unique_ptr<DevH2> assemble(const DevTree& t, int kind, double a, double eps, bool force_general,
                                 int64_t max_rank, cudaStream_t s);
+void release_workspace();  // frees the per-device ACA arenas
 void aca_single(int kind, double a, const double* X, int64_t m, const double* Y, int64_t n, int d, double eps,
                 int64_t cap, double* U, double* V, int64_t* rp, int64_t* cp, int* conv, int64_t* nevals,
                 int64_t* rank);

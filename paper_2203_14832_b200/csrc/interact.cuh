@@ -169,33 +169,6 @@ __device__ __forceinline__ double rsq_seed_f32(double x) {
   return __hiloint2double((int)((unsigned)yb >> 3) + ((1023 - 127) << 20), yb << 29);
 }
 
-// ---- mbarrier / TMA bulk-copy helpers (sm_90+ PTX, used on sm_100a) ----
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-// generic-proxy smem writes (the in-place transform) before a later TMA write
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
 // K(r2) for the interaction kernel, non-1/r kinds (1/r is acc_inv_r).
 template <int KIND>
 __device__ __forceinline__ double kpair(double r2, const KParams& kp) {
@@ -610,17 +583,14 @@ void launch_chunk(const DevH2& h, int64_t R, int64_t r0, const KParams& kp, cuda
   const size_t smem = (sizeof(LevelTab) * ntabs + 127) / 128 * 128 +
                       (IT2 / 32) * sizeof(WarpSmem<D, NR, TILE, (NR == 1 ? H2B_RT : 2)>);
   auto kern = interact_warps<D, KIND, NR, TILE, (NR == 1 ? H2B_RT : 2), F32S>;
-  static int grid = 0;  // per instantiation: persistent grid = resident CTAs
-  static size_t grid_smem = 0;
-  if (grid == 0 || grid_smem != smem) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int dev = 0, nsm = 0, per = 0;
-    CK(cudaGetDevice(&dev));
-    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, IT2, smem));
-    grid = nsm * (per > 0 ? per : 1);
-    grid_smem = smem;
-  }
+  // persistent grid = resident CTAs; attribute and occupancy are per device, so they are set on every call
+  // (a process may drive several GPUs)
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int dev = 0, nsm = 0, per = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, IT2, smem));
+  const int grid = nsm * (per > 0 ? per : 1);
   // pack this chunk's charges into the records
   const auto& pk = NR == 1 ? h.pack1 : h.pack16;
   if (pk.total && !(NR == 1 && R == 1)) {  // one RHS: gather / upward pass already wrote the charges

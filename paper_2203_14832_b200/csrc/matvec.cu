@@ -436,6 +436,19 @@ void build_tabs(DevH2& h, int64_t R, cudaStream_t s) {
 void ensure_scratch(DevH2& h, int64_t R, cudaStream_t s) {
   const DevTree& T = *h.t;
   if (h.scratch_nrhs == R) return;
+  // another RHS width: park the active set (at most 3 parked, oldest dropped) and revive a parked one of width R
+  MatvecScratch& act = static_cast<MatvecScratch&>(h);
+  if (h.scratch_nrhs != 0) {
+    h.parked.push_back(std::move(act));
+    act = MatvecScratch();
+    if (h.parked.size() > 3) h.parked.erase(h.parked.begin());
+  }
+  for (auto it = h.parked.begin(); it != h.parked.end(); ++it)
+    if (it->scratch_nrhs == R) {
+      act = std::move(*it);
+      h.parked.erase(it);
+      return;
+    }
   h.w_sorted.alloc(T.nq * R, &h.mem);
   h.near.alloc(T.np * R, &h.mem);
   h.wout.clear();

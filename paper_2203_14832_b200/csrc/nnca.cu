@@ -27,35 +27,52 @@ namespace h2b {
 
 namespace {
 
+// ring configurations of the persistent ACA kernel (threads per CTA, columns per thread, rows per batch, CTAs
+// per SM): long candidate lists, and short ones (n_max <= H2B_ACA_SMALL_N)
 #ifndef H2B_ACA_NT
 #define H2B_ACA_NT 512
+#endif
+#ifndef H2B_ACA_NC
+#define H2B_ACA_NC 4
+#endif
+#ifndef H2B_ACA_TB
+#define H2B_ACA_TB 4
 #endif
 #ifndef H2B_ACA_MINB
 #define H2B_ACA_MINB 1
 #endif
-#ifndef H2B_ACA_CPT
-#define H2B_ACA_CPT 4
+#ifndef H2B_ACA_NT_S
+#define H2B_ACA_NT_S 128
 #endif
-#ifndef H2B_ACA_TB
-#define H2B_ACA_TB 4  // residual rows per load batch in the fused row pass
+#ifndef H2B_ACA_NC_S
+#define H2B_ACA_NC_S 4
 #endif
-#ifndef H2B_ACA_SLAB_GB
-#define H2B_ACA_SLAB_GB 24
+#ifndef H2B_ACA_TB_S
+#define H2B_ACA_TB_S 4
+#endif
+#ifndef H2B_ACA_MB_S
+#define H2B_ACA_MB_S 4
+#endif
+#ifndef H2B_ACA_CELLS_S
+#define H2B_ACA_CELLS_S 2400  // levels with at least this many cells use the small-CTA configuration
+#endif
+#ifndef H2B_ACA_CELLS_M
+#define H2B_ACA_CELLS_M 600   // ... this many: 256-thread CTAs, two per SM; fewer: one 512-thread CTA per SM
+#endif
+#ifndef H2B_ACA_SLOTS
+#define H2B_ACA_SLOTS 4  // ring depth wanted (bounded by shared memory and ACA_MAX_SLOTS)
+#endif
+#ifndef H2B_ACA_UPREF
+#define H2B_ACA_UPREF 512  // doubles of shared memory kept for U before the ring takes the rest
 #endif
 #ifndef H2B_ACA_SLAB_PAD
 #define H2B_ACA_SLAB_PAD 544
 #endif
-#ifndef H2B_ACA_NT_S
-#define H2B_ACA_NT_S 512
-#endif
-#ifndef H2B_ACA_VSMEM_KB
-#define H2B_ACA_VSMEM_KB 200
-#endif
-
 
 constexpr int ACA_MAX_THREADS = 1024;
 constexpr int ACA_MAX_WARPS = ACA_MAX_THREADS / 32;
 constexpr int XCH = 8;  // cross-product partial sums per pass
+constexpr int ACA_MAX_SLOTS = 6;
 
 struct AcaArgs {
   int kind;
@@ -494,17 +511,57 @@ DBuf<T> upload(const std::vector<T>& h, cudaStream_t s, MemStats* ms = nullptr) 
 // ---------------------------------------------------------------------
 // Persistent level-batched ACA (the setup hot path).
 //
-// One CTA per SM (NT = 512 or 1024 threads) pulls cells from a work queue
-// (largest first).  Its workspace (residual factors U, V, the gathered far
-// candidates, used-row/column flags) is a fixed per-CTA slab reused cell
-// after cell, so the working set of all resident cells (~148 x k x n x 8 B)
-// stays in the 126 MB L2: the ACA re-reads V (k x n) at every step, which in
-// a one-CTA-per-cell launch (thousands of cells resident) went to DRAM.
-// The far candidates of a cell are gathered from its interaction list into
-// the slab once, and the interpolation operator (aca.py:297 / :311) is
-// formed right after the ACA from the same slab.  Pivot arithmetic is
-// unchanged (reference operation order, see aca_kernel).
+// CTAs pull cells from a work queue (largest first).  A CTA's workspace (the
+// residual factors U, V, the gathered far candidates, used-row/column flags)
+// is a fixed per-CTA slab reused cell after cell.  Pivot arithmetic is the
+// reference's (see aca_kernel): every residual entry is
+//     K(x_i, y_j) - U[i,0] V[j,0] - ... - U[i,k-1] V[j,k-1]
+// rounded after every multiply and every subtract, left to right.
+//
+// Row pass (the hot loop: step k re-reads all k previous residual rows):
+// one thread owns NC columns of a column segment and keeps their running
+// entries in registers, while the previous rows V[t][segment] stream through
+// a two-slot shared-memory ring of TB rows each, filled by TMA bulk copies
+// (cp.async.bulk, mbarrier completion; one copy per row, issued by thread 0
+// two batches ahead).  The copies keep TB rows x segment bytes in flight per
+// slot with no registers held, which is what the latency-bound register
+// version lacked (ncu: 16 warps, long-scoreboard stalls, 1.2 TB/s).  The
+// pass also finishes step k - 1 (normalises its raw row, forms the cross
+// products <V[t], V[k-1]> for the stopping test) so V is swept once per step.
+// Kernel families (1/r-like, exp, log) are separate instantiations: the
+// unused libm paths stay out of the loop (instruction-cache misses were 20%
+// of the issue stalls with the runtime switch).
 // ---------------------------------------------------------------------
+enum KClass { KC_INV = 0, KC_EXP = 1, KC_LOG = 2 };
+inline int kind_class(int kind) {
+  switch (kind) {
+    case COULOMB:
+    case LAPLACE:
+    case REG_INVERSE: return KC_INV;
+    case GAUSSIAN:
+    case GAUSSIAN_SCALED:
+    case MATERN: return KC_EXP;
+    default: return KC_LOG;
+  }
+}
+
+// kval_exact restricted to one family (same operations, same roundings)
+template <int KC>
+__device__ __forceinline__ double kval_class(int kind, double a, double r2) {
+  if constexpr (KC == KC_INV) {
+    const double r = __dsqrt_rn(r2);
+    if (kind == REG_INVERSE) return r < a ? __ddiv_rn(r, a) : __ddiv_rn(a, r);
+    return r == 0.0 ? 0.0 : __ddiv_rn(kind == LAPLACE ? INV_FOUR_PI : 1.0, r);
+  } else if constexpr (KC == KC_EXP) {
+    if (kind == GAUSSIAN) return exp(-r2);
+    if (kind == GAUSSIAN_SCALED) return exp(-__dmul_rn(a, r2));
+    return exp(-__dsqrt_rn(r2));
+  } else {
+    if (kind == LOG) return kval_exact(LOG, a, r2);
+    return kval_exact(REG_LOG, a, r2);
+  }
+}
+
 #ifdef H2B_ACA_PROF
 __device__ unsigned long long g_aca_prof[8];
 #define APROF(i)                                                    \
@@ -539,25 +596,33 @@ struct CellJob {
   int which;  // 0: row interpolator from U (rows m); 1: column interpolator from V (rows n)
   double* ws;
   int64_t ws_doubles;  // per CTA
-  int64_t m_max, n_max, f_max, cap_max;
-  int64_t u_slab, v_slab;  // doubles reserved per CTA for U / V (0 when they live in shared memory)
+  int64_t f_max, cap_max;
+  int64_t u_slab, v_slab;  // doubles reserved per CTA for U (cells whose U does not fit in shared memory) / V
+  int64_t u_smem;          // doubles of shared memory for U: cells with cap x m <= u_smem keep U there
+  int slots;               // ring depth (row batches of TB rows x one segment)
   unsigned long long* counter;
 };
 
-template <int D, int NT, int CPT, bool VSMEM, bool USMEM, int MB>
-__global__ void __launch_bounds__(NT, MB) aca_cells(CellJob J) {
+template <int D, int KC, int NT, int NC, int TB, int MB>
+__global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
+  static_assert(TB % 4 == 0, "row batches are reduced four rows at a time");
   constexpr int NW = NT / 32;
-  extern __shared__ double sm[];
+  constexpr int SEG = NT * NC;  // columns per segment (ring row length)
+  extern __shared__ __align__(16) double sm[];
   __shared__ RedScratch rs;
   __shared__ double xt[D], yb[D];
   __shared__ long long s_cell;
   __shared__ int64_t s_mp[NT + 1];   // member prefix (far gather)
   __shared__ int64_t s_mb[NT];       // member range begin
+  __shared__ __align__(8) uint64_t s_full[ACA_MAX_SLOTS];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double* urow = sm;
-  double* vcol = sm + J.cap_max;
-  double* crossv = sm + 2 * J.cap_max;
-  double* crossu = sm + 3 * J.cap_max;
+  double* ring = sm;  // [slots][TB][SEG]
+  double* urow = ring + J.slots * (TB * SEG);
+  double* vcol = urow + J.cap_max;
+  double* crossv = vcol + J.cap_max;
+  double* crossu = crossv + J.cap_max;
+  double* crosspart = crossu + J.cap_max;  // [NW][cap]
+  double* usm = crosspart + NW * J.cap_max;
   double* base = J.ws + (int64_t)blockIdx.x * J.ws_doubles;
   double* Ub = base;
   double* Vb = Ub + J.u_slab;
@@ -566,6 +631,16 @@ __global__ void __launch_bounds__(NT, MB) aca_cells(CellJob J) {
   int64_t* RP = FG + J.f_max;
   int64_t* CP = RP + J.cap_max;
   unsigned char* flags = reinterpret_cast<unsigned char*>(CP + J.cap_max);
+  const int S = J.slots;  // ring depth: S - 1 batches in flight while one is consumed
+  if (tid == 0) {
+    for (int q = 0; q < S; q++) mbar_init(&s_full[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const uint32_t bar0 = smem_u32(&s_full[0]), ring0 = smem_u32(ring);
+  // stream state, uniform over the CTA: next slot to fill, slot to consume and its mbarrier parity, batches in
+  // flight (issued, not yet consumed)
+  int islot = 0, cslot = 0, inflight = 0;
+  uint32_t cpar = 0;
   long long last_ = clock64();
   (void)last_;
   for (;;) {
@@ -637,9 +712,12 @@ __global__ void __launch_bounds__(NT, MB) aca_cells(CellJob J) {
       }
       continue;
     }
-    // shared-memory residents after the 4 cap-sized vectors: U (cap x m) if USMEM, then V (cap x n) if VSMEM
-    double* U = USMEM ? sm + 4 * J.cap_max : Ub;
-    double* V = VSMEM ? sm + 4 * J.cap_max + (USMEM ? cap * m : 0) : Vb;
+    double* U = cap * m <= J.u_smem ? usm : Ub;  // U (cap x m) in shared memory when it fits
+    double* V = Vb;                               // V (cap x ldv) in the slab, rows 16-byte aligned for the bulk copies
+    const int ni = (int)n;
+    const int64_t ldv = (n + 1) & ~(int64_t)1;
+    const int nseg = (ni + SEG - 1) / SEG;
+    const int seglen = (((ni + nseg - 1) / nseg) + 1) & ~1;
     unsigned char* ru = flags;
     unsigned char* cu = flags + m;
     for (int64_t q = tid; q < m + n; q += NT) ru[q] = 0;
@@ -655,14 +733,32 @@ __global__ void __launch_bounds__(NT, MB) aca_cells(CellJob J) {
     // speculative and discarded (with its evaluation count) if step k - 1
     // stops.  Pivots, residual arithmetic and the test are unchanged; only the
     // summation order of the norm bookkeeping differs from the reference.
-    double* crosspart = sm + 4 * J.cap_max + (USMEM ? cap * m : 0) + (VSMEM ? cap * n : 0);  // [NW][cap]
     bool pend = false;          // step k - 1 awaits normalisation + stopping test
     double piv_prev = 1.0, u2_prev = 0.0;
-    const int ni = (int)n;
+    // Batch q of a pass over kfq rows (nbq batches per segment): rows [b TB, b TB + TB) of segment q / nbq.
+    // Thread 0 arms the slot's mbarrier and issues one bulk copy per row; every thread advances the stream state.
+    int pre = 0;  // batches of the next pass already in flight
+    auto issue = [&](int q, int kfq, int nbq) {
+      if (tid == 0) {
+        const int sg = q / nbq, b = q - sg * nbq;
+        const int c0 = sg * seglen;
+        const int len = ni - c0 < seglen ? ni - c0 : seglen;
+        const uint32_t bytes = (uint32_t)((len + 1) & ~1) * 8u;
+        const int r0 = b * TB;
+        const int rows = kfq - r0 < TB ? kfq - r0 : TB;
+        const uint32_t bar = bar0 + 8u * (uint32_t)islot;
+        mbar_expect_tx_u32(bar, (uint32_t)rows * bytes);
+        const double* src = V + (int64_t)r0 * ldv + c0;
+        const uint32_t dst = ring0 + (uint32_t)(islot * TB) * (uint32_t)(SEG * 8);
+        for (int tt = 0; tt < rows; tt++) bulk_g2s_u32(dst + (uint32_t)tt * (uint32_t)(SEG * 8), src + (int64_t)tt * ldv, bytes, bar);
+      }
+      if (++islot == S) islot = 0;
+      inflight++;
+    };
     // normalise row r = k - 1 on its own (and optionally its cross products): used when no fused pass follows
     auto finish_row = [&](int r, bool need_cross) -> double {
       double v2p = 0.0;
-      double* Vr = V + (int64_t)r * n;
+      double* Vr = V + (int64_t)r * ldv;
       for (int j = tid; j < ni; j += NT) {
         const double v = __ddiv_rn(Vr[j], piv_prev);
         Vr[j] = v;
@@ -671,7 +767,7 @@ __global__ void __launch_bounds__(NT, MB) aca_cells(CellJob J) {
       __syncthreads();
       if (need_cross) {
         for (int t = warp; t < r; t += NW) {
-          const double* Vt = V + (int64_t)t * n;
+          const double* Vt = V + (int64_t)t * ldv;
           double s0 = 0.0, s1 = 0.0;
           int j = lane;
           for (; j + 32 < ni; j += 64) {
@@ -702,63 +798,87 @@ __global__ void __launch_bounds__(NT, MB) aca_cells(CellJob J) {
         best = -1.0;
         bj = -1;
         const int ki = (int)k;
-        const int kf = fuse ? ki - 1 : ki;  // rows read as already normalised
+        const int kf = fuse ? ki - 1 : ki;  // rows streamed (already normalised)
+        const int nb = (kf + TB - 1) / TB;
+        const int Q = nseg * nb;  // batches of this pass, streamed in (segment, batch) order
+        int qi = pre;             // ... of which `pre` were issued at the end of the previous pass
+        pre = 0;
+        while (qi < Q && inflight < S) issue(qi++, kf, nb);
         double v2p = 0.0;
-        double* Vlast = V + (int64_t)(ki - 1) * n;
-        // warp-uniform trip count (the fused pass reduces across lanes); columns past n are masked
-        for (int jb = 0; jb < ni; jb += CPT * NT) {
-          const int j0 = jb + tid;
-          double acc[CPT], vl[CPT];
-          int jc[CPT];
-          // all loads of the iteration head first (coordinates, raw row k - 1), then the arithmetic
-          double y[CPT][D], raw[CPT];
+        double* Vlast = V + (int64_t)(ki - 1) * ldv;
+        double* Vnew = V + (int64_t)ki * ldv;
+        for (int sgi = 0; sgi < nseg; sgi++) {
+          const int c0 = sgi * seglen;
+          const int len = ni - c0 < seglen ? ni - c0 : seglen;
+          double acc[NC], vl[NC];
+          bool ok[NC];
+          int off[NC];  // column offset inside a ring row; padding lanes read column 0 (finite, times vl = 0)
+          {
+            // all loads of the segment head first (coordinates, raw row k - 1), then the arithmetic
+            double y[NC][D], raw[NC];
 #pragma unroll
-          for (int c = 0; c < CPT; c++) {
-            const int jj = j0 + c * NT;
-            jc[c] = jj < ni ? jj : 0;
+            for (int c = 0; c < NC; c++) {
+              const int jl = tid + c * NT;
+              ok[c] = jl < len;
+              off[c] = ok[c] ? jl : 0;
+              const int jj = c0 + off[c];
 #pragma unroll
-            for (int q = 0; q < D; q++) y[c][q] = colc(q, jc[c]);
-            raw[c] = fuse ? Vlast[jc[c]] : 0.0;
-          }
+              for (int q = 0; q < D; q++) y[c][q] = colc(q, jj);
+              raw[c] = fuse ? Vlast[jj] : 0.0;
+            }
 #pragma unroll
-          for (int c = 0; c < CPT; c++) {
-            const int jj = j0 + c * NT;
-            acc[c] = jj < ni ? kval_exact(J.kind, J.a, r2_exact<D>(xl, y[c])) : 0.0;  // no work on padding
-            vl[c] = 0.0;
-            if (fuse && jj < ni) {  // normalise row k - 1 in passing
-              vl[c] = __ddiv_rn(raw[c], piv_prev);
-              Vlast[jj] = vl[c];
-              v2p += vl[c] * vl[c];
+            for (int c = 0; c < NC; c++) {
+              acc[c] = ok[c] ? kval_class<KC>(J.kind, J.a, r2_exact<D>(xl, y[c])) : 0.0;  // no work on padding
+              vl[c] = 0.0;
+              if (fuse && ok[c]) {  // normalise row k - 1 in passing
+                vl[c] = __ddiv_rn(raw[c], piv_prev);
+                Vlast[c0 + off[c]] = vl[c];
+                v2p += vl[c] * vl[c];
+              }
             }
           }
-          const double* Vt = V;
-          if (fuse) {
-            // rows t < k - 1 in blocks of TB: all TB x CPT loads issued before the dependent arithmetic
-            constexpr int TB = H2B_ACA_TB;
-            for (int t0 = 0; t0 < kf; t0 += TB, Vt += TB * (int64_t)n) {
-              double v[TB][CPT];
-              const bool fullb = t0 + TB <= kf;
+          for (int b = 0; b < nb; b++) {
+            const int r0 = b * TB;
+            mbar_wait_u32(bar0 + 8u * (uint32_t)cslot, cpar);
+            const double* R = ring + cslot * (TB * SEG);
+            const int rows = kf - r0 < TB ? kf - r0 : TB;
 #pragma unroll
-              for (int tt = 0; tt < TB; tt++)
+            for (int g4 = 0; g4 < TB; g4 += 4) {
+              if (g4 >= rows) break;  // uniform
+              double p[4];
+              if (g4 + 4 <= rows) {  // four whole rows: unconditional loads, then the arithmetic
+                double v[4][NC];
 #pragma unroll
-                for (int c = 0; c < CPT; c++)
-                  v[tt][c] = (fullb || t0 + tt < kf) ? Vt[(int64_t)tt * n + jc[c]] : 0.0;
+                for (int tt = 0; tt < 4; tt++)
 #pragma unroll
-              for (int g4 = 0; g4 < TB; g4 += 4) {
-                double p[4];
+                  for (int c = 0; c < NC; c++) v[tt][c] = R[(g4 + tt) * SEG + off[c]];
+#pragma unroll
+                for (int tt = 0; tt < 4; tt++) {
+                  const double ut = urow[r0 + g4 + tt];
+                  p[tt] = 0.0;
+#pragma unroll
+                  for (int c = 0; c < NC; c++) {
+                    acc[c] = __dsub_rn(acc[c], __dmul_rn(ut, v[tt][c]));
+                    p[tt] = fma(v[tt][c], vl[c], p[tt]);
+                  }
+                }
+              } else {  // last rows of the pass
 #pragma unroll
                 for (int tt = 0; tt < 4; tt++) {
                   p[tt] = 0.0;
-                  if (fullb || t0 + g4 + tt < kf) {
-                    const double ut = urow[t0 + g4 + tt];
+                  if (g4 + tt < rows) {  // uniform
+                    const double ut = urow[r0 + g4 + tt];
 #pragma unroll
-                    for (int c = 0; c < CPT; c++) {
-                      acc[c] = __dsub_rn(acc[c], __dmul_rn(ut, v[g4 + tt][c]));
-                      p[tt] = fma(v[g4 + tt][c], vl[c], p[tt]);
+                    for (int c = 0; c < NC; c++) {
+                      const double v = R[(g4 + tt) * SEG + off[c]];
+                      acc[c] = __dsub_rn(acc[c], __dmul_rn(ut, v));
+                      p[tt] = fma(v, vl[c], p[tt]);
                     }
                   }
                 }
-                // transpose-reduce 4 partial sums over the warp: lane gets t = t0 + g4 + ((lane >> 3) & 3)
+              }
+              if (fuse) {
+                // transpose-reduce 4 partial sums over the warp: lane gets t = r0 + g4 + ((lane >> 3) & 3)
                 const bool b4 = lane & 16, b3 = lane & 8;
                 double k0 = b4 ? p[2] : p[0], k1 = b4 ? p[3] : p[1];
                 k0 += __shfl_xor_sync(0xffffffffu, b4 ? p[0] : p[2], 16);
@@ -768,38 +888,28 @@ __global__ void __launch_bounds__(NT, MB) aca_cells(CellJob J) {
                 kk += __shfl_xor_sync(0xffffffffu, kk, 4);
                 kk += __shfl_xor_sync(0xffffffffu, kk, 2);
                 kk += __shfl_xor_sync(0xffffffffu, kk, 1);
-                const int tq = t0 + g4 + ((lane >> 3) & 3);
+                const int tq = r0 + g4 + ((lane >> 3) & 3);
                 if ((lane & 7) == 0 && tq < kf) crosspart[warp * cap + tq] += kk;
               }
             }
-#pragma unroll
-            for (int c = 0; c < CPT; c++) acc[c] = __dsub_rn(acc[c], __dmul_rn(urow[ki - 1], vl[c]));
-          } else {
-            int t = 0;
-            for (; t + 4 <= ki; t += 4, Vt += 4 * (int64_t)n) {
-              double v[4][CPT];
-#pragma unroll
-              for (int tt = 0; tt < 4; tt++)
-#pragma unroll
-                for (int c = 0; c < CPT; c++) v[tt][c] = Vt[(int64_t)tt * n + jc[c]];
-#pragma unroll
-              for (int tt = 0; tt < 4; tt++) {
-                const double ut = urow[t + tt];
-#pragma unroll
-                for (int c = 0; c < CPT; c++) acc[c] = __dsub_rn(acc[c], __dmul_rn(ut, v[tt][c]));
-              }
+            __syncthreads();  // every thread is done with the slot: it takes the next batch of the stream
+            if (++cslot == S) {
+              cslot = 0;
+              cpar ^= 1u;
             }
-            for (; t < ki; t++, Vt += ni) {
-              const double ut = urow[t];
+            inflight--;
+            if (qi < Q) issue(qi++, kf, nb);
+          }
+          if (fuse) {
+            const double ul = urow[ki - 1];
 #pragma unroll
-              for (int c = 0; c < CPT; c++) acc[c] = __dsub_rn(acc[c], __dmul_rn(ut, Vt[jc[c]]));
-            }
+            for (int c = 0; c < NC; c++) acc[c] = __dsub_rn(acc[c], __dmul_rn(ul, vl[c]));
           }
 #pragma unroll
-          for (int c = 0; c < CPT; c++) {
-            const int jj = j0 + c * NT;
-            if (jj < ni) {
-              V[(int64_t)k * n + jj] = acc[c];
+          for (int c = 0; c < NC; c++) {
+            if (ok[c]) {
+              const int jj = c0 + off[c];
+              Vnew[jj] = acc[c];
               if (!cu[jj]) {
                 const double val = fabs(acc[c]);
                 if (val > best) {
@@ -810,9 +920,17 @@ __global__ void __launch_bounds__(NT, MB) aca_cells(CellJob J) {
             }
           }
         }
+        fence_proxy_async_all();  // the rows written above are read by bulk copies (async proxy) in later passes
         APROF(1);
         if (bj < 0) best = -1.0;
         block_argmax<NT>(best, bj, rs);
+        // The next pass (a retry with another trial row, or step k + 1) streams rows 0 .. k - 1 whatever happens:
+        // start its first batches now, so they fly during the pivot search and the column pass.  (The barriers
+        // inside block_argmax order every thread's row writes + proxy fence before these copies.)
+        if (ki > 0) {
+          const int nbn = (ki + TB - 1) / TB, Qn = nseg * nbn;
+          while (pre < Qn && inflight < S) issue(pre++, ki, nbn);
+        }
         APROF(2);
         if (fuse) {  // finish step k - 1: cross products, norm update, stopping test
           for (int t = tid; t < kf; t += NT) {
@@ -845,9 +963,9 @@ __global__ void __launch_bounds__(NT, MB) aca_cells(CellJob J) {
       }
       if (stop_prev || exhausted) break;
       // pivot of step k; the row stays raw until the next pass normalises it
-      const double piv = V[k * n + bj];
+      const double piv = V[k * ldv + bj];
       if (tid < D) yb[tid] = colc(tid, bj);
-      for (int64_t t = tid; t < k; t += NT) vcol[t] = V[t * n + bj];
+      for (int64_t t = tid; t < k; t += NT) vcol[t] = V[t * ldv + bj];
       __syncthreads();
       if (tid == 0) cu[bj] = 1;
       APROF(3);
@@ -859,7 +977,7 @@ __global__ void __launch_bounds__(NT, MB) aca_cells(CellJob J) {
         double xl[D];
 #pragma unroll
         for (int q = 0; q < D; q++) xl[q] = rowc(q, i);
-        double acc = kval_exact(J.kind, J.a, r2_exact<D>(xl, yl));
+        double acc = kval_class<KC>(J.kind, J.a, r2_exact<D>(xl, yl));
         for (int64_t t = 0; t < k; t++) acc = __dsub_rn(acc, __dmul_rn(U[t * m + i], vcol[t]));
         U[k * m + i] = acc;
         u2p += acc * acc;
@@ -915,6 +1033,15 @@ __global__ void __launch_bounds__(NT, MB) aca_cells(CellJob J) {
       pend = true;
       __syncthreads();
     }
+    // batches prefetched for a pass that never came: consume them so the ring and the parities stay in step
+    for (; pre > 0; pre--) {
+      mbar_wait_u32(bar0 + 8u * (uint32_t)cslot, cpar);
+      if (++cslot == S) {
+        cslot = 0;
+        cpar ^= 1u;
+      }
+      inflight--;
+    }
     __syncthreads();
     APROF(6);
     const int64_t po = J.piv_off[cell];
@@ -928,15 +1055,20 @@ __global__ void __launch_bounds__(NT, MB) aca_cells(CellJob J) {
       J.tpiv[po + t] = J.rows_far ? FG[r] : J.own.gidx[ob + r];
       J.spiv[po + t] = J.rows_far ? J.own.gidx[ob + c] : FG[c];
     }
-    // interpolation operator (interp_kernel, same arithmetic): which 0 -> P = U L^{-1}; 1 -> Q = V R^{-T}
+    // interpolation operator (aca.py:297 / :311, same arithmetic): which 0 -> P = U L^{-1}; 1 -> Q = V R^{-T}.
+    // The back substitution re-reads the columns of P it has already formed: when the operator fits, it is built
+    // in the (now idle) ring and copied out coalesced.
     if (k > 0) {
       const int64_t rows = J.which == 0 ? m : n;
+      const int64_t fs = J.which == 0 ? m : ldv;  // row stride of the factor
       const double* F = J.which == 0 ? U : V;
       const int64_t* pv = J.which == 0 ? RP : CP;
-      double* P = J.mat + J.mat_off[cell];
+      double* Pg = J.mat + J.mat_off[cell];
+      const bool staged = k * rows <= (int64_t)S * TB * SEG;
+      double* P = staged ? ring : Pg;
       for (int64_t i = tid; i < rows; i += NT) {
         for (int64_t sI = k - 1; sI >= 0; sI--) {
-          const double* Fs = F + sI * rows;
+          const double* Fs = F + sI * fs;
           double acc = Fs[i];
           for (int64_t t = sI + 1; t < k; t++) acc -= P[t * rows + i] * Fs[pv[t]];
           P[sI * rows + i] = J.which == 0 ? acc / Fs[pv[sI]] : acc;
@@ -946,6 +1078,11 @@ __global__ void __launch_bounds__(NT, MB) aca_cells(CellJob J) {
       for (int64_t q = tid; q < k * k; q += NT) {
         const int64_t t = q / k, sI = q % k;
         P[sI * rows + pv[t]] = (sI == t) ? 1.0 : 0.0;
+      }
+      if (staged) {
+        __syncthreads();
+        for (int64_t q = tid; q < k * rows; q += NT) Pg[q] = P[q];
+        fence_proxy_async_all();  // generic writes to the ring before the next cell's bulk copies into it
       }
     }
     APROF(7);
@@ -971,29 +1108,43 @@ struct SideResult {
   DBuf<int64_t> mat_off, mat_rows;
 };
 
-// Process-wide ACA workspace arena: grows to the largest launch seen and is
-// reused after that, so repeated setups do not churn the allocator (pool
-// growth in the middle of a setup made some runs 2-3x slower).
-static DBuf<double>& aca_arena_buf() {
-  static DBuf<double> arena;
-  return arena;
+// Per-device ACA workspace arena: grows to the largest launch seen and is reused after that, so repeated setups
+// do not churn the allocator (pool growth in the middle of a setup made some runs 2-3x slower).  Assemblies on
+// one device are serialised by the arena's mutex (each one fills the GPU anyway); h2b_release_workspace() frees
+// the arenas.
+struct DeviceArena {
+  std::mutex mu;
+  DBuf<double> buf;
+};
+DeviceArena* device_arenas() {
+  static DeviceArena arenas[64];
+  return arenas;
 }
-int64_t aca_arena_size() { return (int64_t)aca_arena_buf().n; }
-double* aca_arena(size_t doubles, cudaStream_t s) {
-  DBuf<double>& arena = aca_arena_buf();
-  if (arena.n < doubles) {
+DeviceArena& current_arena() {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  return device_arenas()[dev & 63];
+}
+double* aca_arena(DeviceArena& A, size_t doubles, cudaStream_t s) {
+  if (A.buf.n < doubles) {
     CK(cudaStreamSynchronize(s));
-    arena.release();
-    arena.alloc(doubles + doubles / 8);
+    A.buf.release();
+    A.buf.alloc(doubles + doubles / 8);
   }
-  return arena.get();
+  return A.buf.get();
 }
 
-template <int D>
+// ring configurations: threads per CTA, columns per thread, rows per batch, CTAs per SM
+template <int D, int KC, int NT, int NC, int TB, int MB>
+struct RingCfg {
+  static constexpr int nt = NT, seg = NT * NC, slot = TB * NT * NC, mb = MB;  // slot: doubles per ring slot
+  static auto kern() { return aca_ring<D, KC, NT, NC, TB, MB>; }
+};
+
+template <int D, int KC>
 void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const Src& far, int kind, double a,
-              double eps, int64_t max_rank, int which_interp, SideResult& R, cudaStream_t s) {
+              double eps, int64_t max_rank, int which_interp, SideResult& R, DeviceArena& arena, cudaStream_t s) {
   const auto wall0 = std::chrono::steady_clock::now();
-  constexpr int NT = H2B_ACA_NT, CPT = H2B_ACA_CPT;
   const DevLevel& L = T.lv[level];
   const int64_t n = L.n;
   DBuf<int64_t> own_b, own_len, far_len;
@@ -1062,25 +1213,13 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
     R.rank_h.clear();
     return;
   }
-  // Cells whose ACA factors fit in shared memory run in a U,V-in-smem launch; the rest keep U (cap x m) in
-  // shared memory when it fits and V in the per-CTA global slab.
-  const int64_t sm_budget = H2B_ACA_VSMEM_KB * 1024 / 8 - (4 + 32) * cap_max;  // + per-warp cross partials
-#ifdef H2B_ACA_NO_USMEM
-  const int64_t u_budget = 0;
-#else
-  const int64_t u_budget = sm_budget;
-#endif
-  std::vector<int64_t> small, mid, large;
-  for (int64_t c : order) {
-    if (caph[c] * (nh[c] + mh[c]) <= sm_budget) small.push_back(c);
-    else if (caph[c] * mh[c] <= u_budget) mid.push_back(c);
-    else large.push_back(c);
-  }
   auto d_cap = upload(caph, s);
-  auto d_small = upload(small, s), d_mid = upload(mid, s), d_large = upload(large, s), d_order_all = upload(order, s);
-  int dev = 0, nsm = 0;
+  auto d_order = upload(order, s);
+  int dev = 0, nsm = 0, smem_sm = 0, smem_cta = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+  CK(cudaDeviceGetAttribute(&smem_cta, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const auto wall2 = std::chrono::steady_clock::now();
   CellJob J;
   J.kind = kind;
@@ -1101,63 +1240,73 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
   J.mat = R.mat.get();
   J.mat_off = R.mat_off.get();
   J.which = which_interp;
-  J.m_max = m_max;
   J.f_max = f_max;
   J.cap_max = cap_max;
+  J.ncell = n;
+  J.order = d_order.get();
   static const bool verbose = getenv("H2B_SETUP_VERBOSE") != nullptr;
-  auto launch = [&](auto kern, int nt, const std::vector<int64_t>& cells, const DBuf<int64_t>& d_cells, bool vsmem,
-                    bool usmem) {
-    if (cells.empty()) return;
-    int64_t nmx = 1, res = 0;
-    for (int64_t c : cells) {
-      nmx = std::max(nmx, nh[c]);
-      res = std::max(res, caph[c] * ((usmem ? mh[c] : 0) + (vsmem ? nh[c] : 0)));
+  auto launch = [&](auto cfg) {
+    using C = decltype(cfg);
+    auto kern = C::kern();
+    // shared memory: 4 cap-sized vectors and the per-warp cross partials, then as many ring slots as fit (deep
+    // prefetch hides the DRAM latency of the residual rows), then U for the cells whose cap x m fits in the rest
+    cudaFuncAttributes fa;
+    CK(cudaFuncGetAttributes(&fa, kern));  // static shared memory; every CTA also reserves 1 KB
+    const int64_t vecs = (4 + C::nt / 32) * cap_max;
+    int64_t u_need = 0;
+    for (int64_t c = 0; c < n; c++) u_need = std::max(u_need, caph[c] * mh[c]);
+    const int64_t u_pref = std::min<int64_t>(u_need, H2B_ACA_UPREF);
+    // this CTA's share of the SM at C::mb CTAs per SM; fewer CTAs per SM when two ring slots do not fit in it
+    int64_t share = 0, slots = 0;
+    for (int mb = C::mb; mb >= 1 && slots < 2; mb--) {
+      share = (std::min<int64_t>(smem_cta, smem_sm / mb - 1024) - (int64_t)fa.sharedSizeBytes) / 8 - 16;
+      slots = (share - vecs - u_pref) / C::slot;
+      if (slots < 2) slots = (share - vecs) / C::slot;
     }
-    const size_t smem = (size_t)(4 * cap_max + res + (nt / 32) * cap_max) * sizeof(double);
-    if (smem > 220 * 1024) throw std::runtime_error("ACA rank cap too large for shared memory");
+    if (slots < 2) throw std::runtime_error("ACA rank cap too large for shared memory");
+    slots = std::min<int64_t>(slots, H2B_ACA_SLOTS);
+    J.slots = (int)slots;
+    const int64_t fixed = slots * C::slot + vecs;
+    J.u_smem = std::max<int64_t>(0, std::min<int64_t>(u_need, share - fixed));
+    const size_t smem = (size_t)(fixed + J.u_smem) * sizeof(double);
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, nt, smem));
-    int64_t gmax = (int64_t)nsm * std::max(per, 1);
-    int64_t grid = std::min<int64_t>((int64_t)cells.size(), gmax);
-    J.ncell = (int64_t)cells.size();
-    J.order = d_cells.get();
-    J.n_max = nmx;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, C::nt, smem));
+    int64_t grid = std::min<int64_t>(n, (int64_t)nsm * std::max(per, 1));
     int64_t us = 0, vs = 0;
-    for (int64_t c : cells) {
-      us = std::max(us, caph[c] * mh[c]);
-      vs = std::max(vs, caph[c] * nh[c]);
+    for (int64_t c = 0; c < n; c++) {
+      if (caph[c] * mh[c] > J.u_smem) us = std::max(us, caph[c] * mh[c]);
+      vs = std::max(vs, (caph[c] + 1) * ((nh[c] + 1) & ~(int64_t)1));  // + 1: the speculative last row pass
     }
-    J.u_slab = usmem ? 0 : us;
-    J.v_slab = vsmem ? 0 : vs;
+    J.u_slab = (us + 1) & ~(int64_t)1;
+    J.v_slab = vs;
     int64_t ws = J.u_slab + J.v_slab + D * f_max + f_max + 2 * cap_max + (m_max + n_max + 7) / 8 + 1;
     ws = (ws + 31) / 32 * 32 + H2B_ACA_SLAB_PAD;  // pad: per-CTA slabs off power-of-two strides
-    if (grid * ws > aca_arena_size()) {
+    if (grid * ws > (int64_t)arena.buf.n) {
       // Slabs are sized for the rank cap (min(m, n)): the top levels of dense clouds (n ~ 1e5 candidates per
       // cell) need ~0.8 GB per concurrent cell, so their total is bounded by the memory available (device free
       // memory + the unused part of the reserved pool) -- fewer concurrent cells instead of running out.  An
       // arena that already holds >= 3/4 of the wanted slabs is used as is: growing it means mapping tens of GB
       // again (measured 650 ms at c1) for a <= 25% longer launch.  Steady-state setups skip the query.
-      const int64_t have = aca_arena_size() / ws;
+      const int64_t have = (int64_t)arena.buf.n / ws;
       if (have >= 1 && 4 * have >= 3 * grid) {
         grid = have;
       } else {
         size_t fr = 0, tot = 0;
         CK(cudaMemGetInfo(&fr, &tot));
         size_t pool_free = 0;
-        int dv = 0;
         cudaMemPool_t pool;
-        if (cudaGetDevice(&dv) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dv) == cudaSuccess) {
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
           uint64_t rsv = 0, used = 0;
           if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &rsv) == cudaSuccess &&
               cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess && rsv > used)
             pool_free = (size_t)(rsv - used);
         }
-        const int64_t budget = (int64_t)(0.6 * (double)(fr + pool_free) / sizeof(double)) + aca_arena_size();
+        const int64_t budget = (int64_t)(0.6 * (double)(fr + pool_free) / sizeof(double)) + (int64_t)arena.buf.n;
         grid = std::max<int64_t>(1, std::min<int64_t>(grid, budget / ws));
       }
     }
-    double* wsbuf = aca_arena((size_t)(grid * ws), s);
+    double* wsbuf = aca_arena(arena, (size_t)(grid * ws), s);
     DBuf<unsigned long long> counter;
     counter.alloc(1);
     CK(cudaMemsetAsync(counter.get(), 0, sizeof(unsigned long long), s));
@@ -1170,16 +1319,18 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
       CK(cudaEventCreate(&e1));
       CK(cudaEventRecord(e0, s));
     }
-    kern<<<(unsigned)grid, nt, smem, s>>>(J);
+    kern<<<(unsigned)grid, C::nt, smem, s>>>(J);
     CKL();
     if (verbose) {
       CK(cudaEventRecord(e1, s));
       CK(cudaEventSynchronize(e1));
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, e0, e1));
-      fprintf(stderr, "[h2b] level %d side %d %s: %zu cells, m_max %lld n_max %lld cap_max %lld, grid %lld x %d: %.3f ms\n",
-              level, which_interp, vsmem ? "UV-smem" : (usmem ? "U-smem" : "global"), cells.size(), (long long)m_max, (long long)nmx,
-              (long long)cap_max, (long long)grid, nt, ms);
+      fprintf(stderr,
+              "[h2b] level %d side %d: %lld cells, m_max %lld n_max %lld cap_max %lld, grid %lld x %d (%d per SM), "
+              "segment %d x %d slots, smem %zu B (U %lld doubles): %.3f ms\n",
+              level, which_interp, (long long)n, (long long)m_max, (long long)n_max, (long long)cap_max,
+              (long long)grid, C::nt, per, C::seg, J.slots, smem, (long long)J.u_smem, ms);
       cudaEventDestroy(e0);
       cudaEventDestroy(e1);
 #ifdef H2B_ACA_PROF
@@ -1193,25 +1344,26 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
 #endif
     }
   };
-  // V in shared memory: one 512-thread CTA per SM; V in the slab: H2B_ACA_NT threads x H2B_ACA_MINB CTAs
-  // per SM (several cells in flight per SM hide the row pass's memory latency)
-  launch(aca_cells<D, H2B_ACA_NT_S, CPT, true, true, 1>, H2B_ACA_NT_S, small, d_small, true, true);
-  launch(aca_cells<D, NT, CPT, false, true, H2B_ACA_MINB>, NT, mid, d_mid, false, true);
-  launch(aca_cells<D, NT, CPT, false, false, H2B_ACA_MINB>, NT, large, d_large, false, false);
+  // Many cells: small CTAs, several per SM (independent cells hide each other's barriers and latencies); few
+  // cells (upper levels): wide CTAs so one cell's row pass uses the whole SM.
+  if (n >= H2B_ACA_CELLS_S) launch(RingCfg<D, KC, H2B_ACA_NT_S, H2B_ACA_NC_S, H2B_ACA_TB_S, H2B_ACA_MB_S>{});
+  else if (n >= H2B_ACA_CELLS_M) launch(RingCfg<D, KC, 256, 4, 4, 2>{});
+  else launch(RingCfg<D, KC, H2B_ACA_NT, H2B_ACA_NC, H2B_ACA_TB, H2B_ACA_MINB>{});
   CK(cudaStreamSynchronize(s));
   const auto wall3 = std::chrono::steady_clock::now();
   R.rank_h = to_host(R.rank.get(), n, s);
-  if (getenv("H2B_SETUP_VERBOSE")) {
+  if (verbose) {
     auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
     fprintf(stderr, "[h2b] level %d side %d: run_side wall %.3f ms (sizes %.3f, host prep %.3f, ACA %.3f, tail %.3f)\n",
             level, which_interp, ms(wall0, std::chrono::steady_clock::now()), ms(wall0, wall1), ms(wall1, wall2),
             ms(wall2, wall3), ms(wall3, std::chrono::steady_clock::now()));
   }
 }
-
-template <int D>
+template <int D, int KC>
 std::unique_ptr<DevH2> assemble_impl(const DevTree& T, int kind, double a, double eps, bool force_general,
                                      int64_t max_rank, cudaStream_t s) {
+  DeviceArena& arena = current_arena();
+  std::lock_guard<std::mutex> arena_lock(arena.mu);  // one assembly per device at a time (shared workspace)
   auto t0 = std::chrono::steady_clock::now();
   auto H = std::make_unique<DevH2>();
   H->t = &T;
@@ -1241,7 +1393,7 @@ std::unique_ptr<DevH2> assemble_impl(const DevTree& T, int kind, double a, doubl
     far_s = own_s;
     // incoming: rows = own targets, cols = far sources
     SideResult in;
-    run_side<D>(T, level, false, own_t, far_s, kind, a, eps, max_rank, 0, in, s);
+    run_side<D, KC>(T, level, false, own_t, far_s, kind, a, eps, max_rank, 0, in, arena, s);
     HL.kin = std::move(in.rank);
     {  // pivot offsets from the ranks already on the host (no device scan + read-back)
       std::vector<int64_t> ptr(HL.n + 1, 0);
@@ -1269,7 +1421,7 @@ std::unique_ptr<DevH2> assemble_impl(const DevTree& T, int kind, double a, doubl
     if (!H->symmetric) {
       // outgoing: rows = far targets, cols = own sources
       SideResult out;
-      run_side<D>(T, level, true, own_s, far_t, kind, a, eps, max_rank, 1, out, s);
+      run_side<D, KC>(T, level, true, own_s, far_t, kind, a, eps, max_rank, 1, out, arena, s);
       HL.kout = std::move(out.rank);
       HL.out_ptr.alloc(HL.n + 1, &H->mem);
       excl_scan(HL.kout.get(), HL.n, HL.out_ptr.get(), s);
@@ -1366,12 +1518,33 @@ std::unique_ptr<DevH2> assemble(const DevTree& t, int kind, double a, double eps
                                 int64_t max_rank, cudaStream_t s) {
   if (!(eps > 0)) throw std::invalid_argument("epsilon must be positive");
   if (!kind_valid(kind)) throw std::invalid_argument("unknown kernel kind");
-  switch (t.d) {
-    case 1: return assemble_impl<1>(t, kind, a, eps, force_general, max_rank, s);
-    case 2: return assemble_impl<2>(t, kind, a, eps, force_general, max_rank, s);
-    case 3: return assemble_impl<3>(t, kind, a, eps, force_general, max_rank, s);
-    default: return assemble_impl<4>(t, kind, a, eps, force_general, max_rank, s);
+#define H2B_ASM(D)                                                                              \
+  switch (kind_class(kind)) {                                                                   \
+    case KC_INV: return assemble_impl<D, KC_INV>(t, kind, a, eps, force_general, max_rank, s); \
+    case KC_EXP: return assemble_impl<D, KC_EXP>(t, kind, a, eps, force_general, max_rank, s); \
+    default: return assemble_impl<D, KC_LOG>(t, kind, a, eps, force_general, max_rank, s);     \
   }
+  switch (t.d) {
+    case 1: H2B_ASM(1)
+    case 2: H2B_ASM(2)
+    case 3: H2B_ASM(3)
+    default: H2B_ASM(4)
+  }
+#undef H2B_ASM
+}
+
+void release_workspace() {
+  int cur = 0, ndev = 0;
+  if (cudaGetDevice(&cur) != cudaSuccess || cudaGetDeviceCount(&ndev) != cudaSuccess) return;
+  for (int dv = 0; dv < ndev && dv < 64; dv++) {
+    DeviceArena& A = device_arenas()[dv];
+    std::lock_guard<std::mutex> g(A.mu);
+    if (!A.buf.n) continue;
+    CK(cudaSetDevice(dv));
+    CK(cudaDeviceSynchronize());
+    A.buf.release();
+  }
+  CK(cudaSetDevice(cur));
 }
 
 // Single-block ACA for the drop-in partial_aca path (_core.pyx:70).

@@ -100,9 +100,50 @@ def dense_rows(kernel: KernelSpec, cloud, rows, w) -> np.ndarray:
     w = _lib.f64(w)
     u = np.empty(rows.size)
     P, Q = cloud.points_p, cloud.points_q
-    _lib.check(_lib.lib().h2b_dense_rows(kernel.kind, kernel.device_param, _lib.dptr(P), _lib.iptr(rows), rows.size,
-                                         _lib.dptr(Q), Q.shape[0], P.shape[1], _lib.dptr(w), _lib.dptr(u)))
+    if rows.size and (rows.min() < 0 or rows.max() >= P.shape[0]):
+        raise IndexError(f"row index out of range for {P.shape[0]} targets")  # the reference's fancy index raises
+    _lib.check(_lib.lib().h2b_dense_rows(kernel.kind, kernel.device_param, _lib.dptr(P), P.shape[0], _lib.iptr(rows),
+                                         rows.size, _lib.dptr(Q), Q.shape[0], P.shape[1], _lib.dptr(w),
+                                         _lib.dptr(u)))
     return u
+
+
+class _PinnedBlock:
+    """Owner of one cudaHostAlloc block; freed when the last numpy view goes away."""
+
+    def __init__(self, nbytes: int):
+        import ctypes
+
+        self.ptr = ctypes.c_void_p()
+        _lib.check(_lib.lib().h2b_host_alloc(ctypes.byref(self.ptr), int(nbytes)))
+        self.nbytes = int(nbytes)
+
+    def __del__(self):
+        try:
+            _lib.lib().h2b_host_free(self.ptr)
+        except Exception:  # interpreter shutdown
+            pass
+
+
+def pinned_empty(shape) -> np.ndarray:
+    """float64 numpy array in page-locked host memory (cudaHostAlloc).
+
+    ``h2_matvec(h2, w)`` with numpy ``w`` / ``out`` allocated here copies at the full PCIe rate and matches the
+    end-to-end time quoted for pinned buffers; ordinary (pageable) numpy arrays go through the driver's staging.
+    """
+    import ctypes
+
+    shape = (int(shape),) if np.isscalar(shape) else tuple(int(x) for x in shape)
+    n = int(np.prod(shape, dtype=np.int64))
+    block = _PinnedBlock(max(n, 1) * 8)
+    buf = (ctypes.c_double * max(n, 1)).from_address(block.ptr.value)
+    buf._h2b_owner = block  # the ctypes array is the numpy array's base: keeps the block alive
+    return np.frombuffer(buf, dtype=np.float64, count=n).reshape(shape)
+
+
+def release_workspace() -> None:
+    """Free the per-device ACA workspace arenas the engine keeps between assemblies."""
+    _lib.check(_lib.lib().h2b_release_workspace())
 
 
 def relative_error(u, u_ref) -> float:

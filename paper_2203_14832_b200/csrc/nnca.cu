@@ -547,11 +547,11 @@ inline int kind_class(int kind) {
 
 // kval_exact restricted to one family (same operations, same roundings)
 template <int KC>
-__device__ __forceinline__ double kval_class(int kind, double a, double r2) {
-  if constexpr (KC == KC_INV) {
+__device__ __forceinline__ double kval_class(int kind, double a, double num, double r2) {
+  if constexpr (KC == KC_INV) {  // num: numerator of the 1/r kernels (1 or 1/(4 pi)), hoisted by the caller
     const double r = __dsqrt_rn(r2);
     if (kind == REG_INVERSE) return r < a ? __ddiv_rn(r, a) : __ddiv_rn(a, r);
-    return r == 0.0 ? 0.0 : __ddiv_rn(kind == LAPLACE ? INV_FOUR_PI : 1.0, r);
+    return r == 0.0 ? 0.0 : __ddiv_rn(num, r);
   } else if constexpr (KC == KC_EXP) {
     if (kind == GAUSSIAN) return exp(-r2);
     if (kind == GAUSSIAN_SCALED) return exp(-__dmul_rn(a, r2));
@@ -600,6 +600,7 @@ struct CellJob {
   int64_t u_slab, v_slab;  // doubles reserved per CTA for U (cells whose U does not fit in shared memory) / V
   int64_t u_smem;          // doubles of shared memory for U: cells with cap x m <= u_smem keep U there
   int slots;               // ring depth (row batches of TB rows x one segment)
+  int bit_words;           // 32-bit words of shared memory for the used-row / used-column bit masks (0: slab bytes)
   unsigned long long* counter;
 };
 
@@ -622,7 +623,9 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
   double* crossv = vcol + J.cap_max;
   double* crossu = crossv + J.cap_max;
   double* crosspart = crossu + J.cap_max;  // [NW][cap]
-  double* usm = crosspart + NW * J.cap_max;
+  // used-row / used-column flags: bit masks in shared memory when they fit (J.bit_words > 0), else bytes in the slab
+  uint32_t* bits = reinterpret_cast<uint32_t*>(crosspart + NW * J.cap_max);
+  double* usm = reinterpret_cast<double*>(bits + J.bit_words);
   double* base = J.ws + (int64_t)blockIdx.x * J.ws_doubles;
   double* Ub = base;
   double* Vb = Ub + J.u_slab;
@@ -631,6 +634,7 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
   int64_t* RP = FG + J.f_max;
   int64_t* CP = RP + J.cap_max;
   unsigned char* flags = reinterpret_cast<unsigned char*>(CP + J.cap_max);
+  const double knum = J.kind == LAPLACE ? INV_FOUR_PI : 1.0;
   const int S = J.slots;  // ring depth: S - 1 batches in flight while one is consumed
   if (tid == 0) {
     for (int q = 0; q < S; q++) mbar_init(&s_full[q], 1);
@@ -720,7 +724,16 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
     const int seglen = (((ni + nseg - 1) / nseg) + 1) & ~1;
     unsigned char* ru = flags;
     unsigned char* cu = flags + m;
-    for (int64_t q = tid; q < m + n; q += NT) ru[q] = 0;
+    const bool sbits = J.bit_words > 0;
+    uint32_t* rbits = bits;
+    uint32_t* cbits = bits + ((m + 31) >> 5);
+    if (sbits) {
+      for (int64_t q = tid; q < ((m + 31) >> 5) + ((n + 31) >> 5); q += NT) bits[q] = 0u;
+    } else {
+      for (int64_t q = tid; q < m + n; q += NT) ru[q] = 0;
+    }
+    auto row_used = [&](int64_t i) -> bool { return sbits ? (rbits[i >> 5] >> (i & 31)) & 1u : ru[i] != 0; };
+    auto col_used = [&](int64_t j) -> bool { return sbits ? (cbits[j >> 5] >> (j & 31)) & 1u : cu[j] != 0; };
     const int64_t full = m < n ? m : n;
     int64_t k = 0, trial = 0, nev = 0;
     double norm2 = 0.0;
@@ -786,7 +799,10 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
       double best;
       int64_t bj;
       for (;;) {
-        if (tid == 0) ru[trial] = 1;
+        if (tid == 0) {
+          if (sbits) rbits[trial >> 5] |= 1u << (trial & 31);
+          else ru[trial] = 1;
+        }
         for (int64_t t = tid; t < k; t += NT) urow[t] = U[t * m + trial];
         if (tid < D) xt[tid] = rowc(tid, trial);
         if (fuse)
@@ -828,7 +844,7 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
             }
 #pragma unroll
             for (int c = 0; c < NC; c++) {
-              acc[c] = ok[c] ? kval_class<KC>(J.kind, J.a, r2_exact<D>(xl, y[c])) : 0.0;  // no work on padding
+              acc[c] = ok[c] ? kval_class<KC>(J.kind, J.a, knum, r2_exact<D>(xl, y[c])) : 0.0;  // no work on padding
               vl[c] = 0.0;
               if (fuse && ok[c]) {  // normalise row k - 1 in passing
                 vl[c] = __ddiv_rn(raw[c], piv_prev);
@@ -910,7 +926,7 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
             if (ok[c]) {
               const int jj = c0 + off[c];
               Vnew[jj] = acc[c];
-              if (!cu[jj]) {
+              if (!col_used(jj)) {
                 const double val = fabs(acc[c]);
                 if (val > best) {
                   best = val;
@@ -952,7 +968,7 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
         if (best > 0.0) break;
         int64_t first = INT64_MAX;
         for (int64_t i = tid; i < m; i += NT)
-          if (!ru[i] && i < first) first = i;
+          if (!row_used(i) && i < first) first = i;
         first = block_min<NT>(first, rs);
         if (first == INT64_MAX) {
           exhausted = true;
@@ -967,7 +983,10 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
       if (tid < D) yb[tid] = colc(tid, bj);
       for (int64_t t = tid; t < k; t += NT) vcol[t] = V[t * ldv + bj];
       __syncthreads();
-      if (tid == 0) cu[bj] = 1;
+      if (tid == 0) {
+        if (sbits) cbits[bj >> 5] |= 1u << (bj & 31);
+        else cu[bj] = 1;
+      }
       APROF(3);
       double yl[D];
 #pragma unroll
@@ -977,7 +996,7 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
         double xl[D];
 #pragma unroll
         for (int q = 0; q < D; q++) xl[q] = rowc(q, i);
-        double acc = kval_class<KC>(J.kind, J.a, r2_exact<D>(xl, yl));
+        double acc = kval_class<KC>(J.kind, J.a, knum, r2_exact<D>(xl, yl));
         for (int64_t t = 0; t < k; t++) acc = __dsub_rn(acc, __dmul_rn(U[t * m + i], vcol[t]));
         U[k * m + i] = acc;
         u2p += acc * acc;
@@ -1016,7 +1035,7 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
       int64_t bi = -1;
       const double* Uk = U + (k - 1) * m;
       for (int64_t i = tid; i < m; i += NT)
-        if (!ru[i]) {
+        if (!row_used(i)) {
           const double val = fabs(Uk[i]);
           if (val > best) {
             best = val;
@@ -1252,7 +1271,10 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
     // prefetch hides the DRAM latency of the residual rows), then U for the cells whose cap x m fits in the rest
     cudaFuncAttributes fa;
     CK(cudaFuncGetAttributes(&fa, kern));  // static shared memory; every CTA also reserves 1 KB
-    const int64_t vecs = (4 + C::nt / 32) * cap_max;
+    int64_t bit_words = (((m_max + 31) >> 5) + ((n_max + 31) >> 5) + 3) & ~(int64_t)1;
+    if (bit_words > 4096) bit_words = 0;  // very long candidate lists keep byte flags in the slab
+    J.bit_words = (int)bit_words;
+    const int64_t vecs = (4 + C::nt / 32) * cap_max + bit_words / 2;
     int64_t u_need = 0;
     for (int64_t c = 0; c < n; c++) u_need = std::max(u_need, caph[c] * mh[c]);
     const int64_t u_pref = std::min<int64_t>(u_need, H2B_ACA_UPREF);

@@ -80,6 +80,10 @@ int64_t h2b_h2_get_i64(const h2b_h2* h, int level, int what, int64_t* dst);
  * row interpolator (l2p for leaves, stacked l2l blocks otherwise), 1 =
  * column interpolator (p2m / stacked m2m^T).  Row-major copy to dst. */
 int64_t h2b_h2_get_interp(const h2b_h2* h, int level, int64_t cell, int which, int64_t* cols, double* dst);
+/* Coefficient vectors of the last single-vector product (matvec.py:169 h2_matvec_reference(collect=True)):
+ * which 0 = w_out (outgoing, after P2M / M2M), 1 = u_in (incoming, after M2L and L2L), cells concatenated in the
+ * reference order, k_out / k_in entries per cell.  Returns the element count; copies when dst != 0. */
+int64_t h2b_h2_get_coeffs(h2b_h2* h, int level, int which, double* dst);
 /* stats[0..9]: evals_pivots evals_couplings evals_nearfield max_rank
  * cells_visited memory_bytes symmetric setup_ns depth aca_unconverged */
 int h2b_h2_stats(const h2b_h2* h, int64_t* stats);

@@ -62,6 +62,8 @@ def _declare(L):
     L.h2b_h2_get_interp.argtypes = [_vp, ctypes.c_int, ctypes.c_int64, ctypes.c_int, _i64p, _dp]
     L.h2b_h2_get_interp.restype = ctypes.c_int64
     L.h2b_h2_stats.argtypes = [_vp, _i64p]
+    L.h2b_h2_get_coeffs.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _dp]
+    L.h2b_h2_get_coeffs.restype = ctypes.c_int64
     L.h2b_matvec.argtypes = [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, _vp]
     L.h2b_matvec_launches.argtypes = [_vp, ctypes.c_int64]
     L.h2b_matvec_launches.restype = ctypes.c_int64
@@ -95,7 +97,7 @@ EXPORTS = (
     "h2b_tree_free", "h2b_tree_info", "h2b_tree_ncells", "h2b_tree_get", "h2b_assemble", "h2b_h2_free",
     "h2b_h2_get_i64", "h2b_h2_get_interp", "h2b_h2_stats", "h2b_matvec", "h2b_matvec_launches",
     "h2b_set_profiling", "h2b_last_stage_ms", "h2b_fp64_peak", "h2b_dense_matvec", "h2b_dense_rows",
-    "h2b_host_alloc", "h2b_host_free", "h2b_release_workspace",
+    "h2b_host_alloc", "h2b_host_free", "h2b_release_workspace", "h2b_h2_get_coeffs",
 )
 
 

@@ -288,8 +288,24 @@ class H2Matrix:
         return self.matvec(w)
 
     def memory_bytes(self) -> int:
-        """Device bytes held by the representation (pivots, coordinates, transfer operators)."""
+        """Device bytes held by the representation (pivots, coordinates, transfer operators, matvec scratch).
+
+        Not comparable with the reference's figure: the engine stores no coupling and no near-field blocks (it
+        regenerates their entries in registers); ``reference_memory_bytes`` is the reference's count.
+        """
         return int(self.native_stats()[5])
+
+    def reference_memory_bytes(self) -> int:
+        """Bytes the reference's representation of this matrix holds (compress.py:142 memory_bytes, before its
+        apply plan is built): stored coupling and near-field blocks, dense transfer operators, pivot index arrays."""
+        st = self.native_stats()
+        total = 8 * (int(st[1]) + int(st[2]))
+        for level in self.compressed_levels():
+            k_in, k_out = self.array(level, "k_in"), self.array(level, "k_out")
+            m_in, n_out = self.array(level, "m_in"), self.array(level, "n_out")
+            total += 8 * int((m_in * k_in).sum() + (n_out * k_out).sum())
+            total += 8 * int(2 * k_in.sum() + 2 * k_out.sum())
+        return total
 
 
 def candidate_sets(cell: Cell, pivots: dict) -> Candidates:

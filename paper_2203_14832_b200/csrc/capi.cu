@@ -388,6 +388,41 @@ int64_t h2b_h2_get_interp(const h2b_h2* hc, int level, int64_t cell, int which, 
   return rc ? rc : ret;
 }
 
+int64_t h2b_h2_get_coeffs(h2b_h2* hc, int level, int which, double* dst) {
+  int64_t ret = 0;
+  int rc = guarded([&] {
+    std::lock_guard<std::mutex> g(hc->mu);
+    DevH2& h = *hc->h;
+    if (which != 0 && which != 1) throw std::invalid_argument("bad field");
+    if (level < 2 || level > h.t->depth) {
+      ret = 0;
+      return;
+    }
+    if (h.last_nrhs != 1 || h.scratch_nrhs != 1)
+      throw std::invalid_argument("the last product on this matrix was not a single-vector product");
+    if (hc->tail.ev) CK(cudaEventSynchronize(hc->tail.ev));
+    h2b_tree* T = hc->tree;
+    {
+      std::lock_guard<std::mutex> gt(T->mu);
+      ensure_perm(T, level);
+    }
+    const auto& perm = T->perm[level];
+    const DevH2Level& L = h.lv[level];
+    const int64_t tot = which == 0 ? L.out_total : L.in_total;
+    auto ptr = to_host(which == 0 ? L.out_ptrd() : L.in_ptr.get(), L.n + 1, 0);
+    auto val = to_host((which == 0 ? h.wout[level] : h.uin[level]).get(), tot, 0);
+    if (dst) {
+      int64_t w = 0;
+      for (int64_t i = 0; i < L.n; i++) {
+        const int64_t c = perm[i];
+        for (int64_t q = ptr[c]; q < ptr[c + 1]; q++) dst[w++] = val[q];
+      }
+    }
+    ret = tot;
+  });
+  return rc ? rc : ret;
+}
+
 int h2b_h2_stats(const h2b_h2* hc, int64_t* st) {
   return guarded([&] {
     const DevH2& h = *hc->h;

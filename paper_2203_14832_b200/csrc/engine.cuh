@@ -114,6 +114,7 @@ struct DevH2 : MatvecScratch {
   std::vector<DevH2Level> lv;  // indexed by level; levels < 2 empty
   int64_t evals_pivots = 0, evals_couplings = 0, evals_nearfield = 0, max_rank = 0, cells_visited = 0;
   int64_t setup_ns = 0, unconverged = 0;
+  int64_t last_nrhs = 0;  // RHS width of the last product (its coefficient vectors are still in wout / uin)
   // matvec scratch of other RHS widths (most recently used last; at most 3 parked)
   std::vector<MatvecScratch> parked;
   DBuf<double> io_w, io_u;  // device staging for host-pointer calls

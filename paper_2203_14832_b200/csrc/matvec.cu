@@ -551,6 +551,7 @@ void matvec(DevH2& h, const double* w, double* u, int64_t R, cudaStream_t s) {
   const DevTree& T = *h.t;
   const int L = T.depth, d = T.d;
   ensure_scratch(h, R, s);
+  h.last_nrhs = R;
   KParams kp = make_kp(h.kind, h.a);
   std::vector<std::pair<int64_t, int>> chunks;
   rhs_chunks(R, chunks);

@@ -73,6 +73,7 @@ constexpr int ACA_MAX_THREADS = 1024;
 constexpr int ACA_MAX_WARPS = ACA_MAX_THREADS / 32;
 constexpr int XCH = 8;  // cross-product partial sums per pass
 constexpr int ACA_MAX_SLOTS = 6;
+constexpr int ACA_BIT_WORDS = 2048;  // used-row / used-column bit masks: rows + columns up to ~65K per cell
 
 struct AcaArgs {
   int kind;
@@ -600,7 +601,7 @@ struct CellJob {
   int64_t u_slab, v_slab;  // doubles reserved per CTA for U (cells whose U does not fit in shared memory) / V
   int64_t u_smem;          // doubles of shared memory for U: cells with cap x m <= u_smem keep U there
   int slots;               // ring depth (row batches of TB rows x one segment)
-  int bit_words;           // 32-bit words of shared memory for the used-row / used-column bit masks (0: slab bytes)
+  int bit_words;           // > 0: used-row / used-column flags are bit masks in shared memory (else bytes in the slab)
   unsigned long long* counter;
 };
 
@@ -623,9 +624,11 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
   double* crossv = vcol + J.cap_max;
   double* crossu = crossv + J.cap_max;
   double* crosspart = crossu + J.cap_max;  // [NW][cap]
-  // used-row / used-column flags: bit masks in shared memory when they fit (J.bit_words > 0), else bytes in the slab
-  uint32_t* bits = reinterpret_cast<uint32_t*>(crosspart + NW * J.cap_max);
-  double* usm = reinterpret_cast<double*>(bits + J.bit_words);
+  // used-row / used-column flags: bit masks in (static) shared memory when they fit (J.bit_words > 0), else bytes
+  // in the slab
+  __shared__ uint32_t s_bits[ACA_BIT_WORDS];
+  uint32_t* bits = s_bits;
+  double* usm = crosspart + NW * J.cap_max;
   double* base = J.ws + (int64_t)blockIdx.x * J.ws_doubles;
   double* Ub = base;
   double* Vb = Ub + J.u_slab;
@@ -1264,7 +1267,7 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
   J.ncell = n;
   J.order = d_order.get();
   static const bool verbose = getenv("H2B_SETUP_VERBOSE") != nullptr;
-  auto launch = [&](auto cfg) {
+  auto launch = [&](auto cfg) -> bool {  // false: the rank cap does not fit this configuration's shared memory
     using C = decltype(cfg);
     auto kern = C::kern();
     // shared memory: 4 cap-sized vectors and the per-warp cross partials, then as many ring slots as fit (deep
@@ -1272,9 +1275,9 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
     cudaFuncAttributes fa;
     CK(cudaFuncGetAttributes(&fa, kern));  // static shared memory; every CTA also reserves 1 KB
     int64_t bit_words = (((m_max + 31) >> 5) + ((n_max + 31) >> 5) + 3) & ~(int64_t)1;
-    if (bit_words > 4096) bit_words = 0;  // very long candidate lists keep byte flags in the slab
+    if (bit_words > ACA_BIT_WORDS) bit_words = 0;  // very long candidate lists keep byte flags in the slab
     J.bit_words = (int)bit_words;
-    const int64_t vecs = (4 + C::nt / 32) * cap_max + bit_words / 2;
+    const int64_t vecs = (4 + C::nt / 32) * cap_max;
     int64_t u_need = 0;
     for (int64_t c = 0; c < n; c++) u_need = std::max(u_need, caph[c] * mh[c]);
     const int64_t u_pref = std::min<int64_t>(u_need, H2B_ACA_UPREF);
@@ -1285,7 +1288,7 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
       slots = (share - vecs - u_pref) / C::slot;
       if (slots < 2) slots = (share - vecs) / C::slot;
     }
-    if (slots < 2) throw std::runtime_error("ACA rank cap too large for shared memory");
+    if (slots < 2) return false;
     slots = std::min<int64_t>(slots, H2B_ACA_SLOTS);
     J.slots = (int)slots;
     const int64_t fixed = slots * C::slot + vecs;
@@ -1365,12 +1368,20 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
       CK(cudaMemcpyToSymbol(g_aca_prof, z, sizeof z));
 #endif
     }
+    return true;
   };
   // Many cells: small CTAs, several per SM (independent cells hide each other's barriers and latencies); few
   // cells (upper levels): wide CTAs so one cell's row pass uses the whole SM.
-  if (n >= H2B_ACA_CELLS_S) launch(RingCfg<D, KC, H2B_ACA_NT_S, H2B_ACA_NC_S, H2B_ACA_TB_S, H2B_ACA_MB_S>{});
-  else if (n >= H2B_ACA_CELLS_M) launch(RingCfg<D, KC, 256, 4, 4, 2>{});
-  else launch(RingCfg<D, KC, H2B_ACA_NT, H2B_ACA_NC, H2B_ACA_TB, H2B_ACA_MINB>{});
+  // The per-warp vectors scale with the rank cap: a cap too large for the preferred configuration falls back to
+  // the narrower ones (fewer warps, smaller ring slots).
+  auto small = [&] { return launch(RingCfg<D, KC, H2B_ACA_NT_S, H2B_ACA_NC_S, H2B_ACA_TB_S, H2B_ACA_MB_S>{}); };
+  auto mid = [&] { return launch(RingCfg<D, KC, 256, 4, 4, 2>{}); };
+  auto wide = [&] { return launch(RingCfg<D, KC, H2B_ACA_NT, H2B_ACA_NC, H2B_ACA_TB, H2B_ACA_MINB>{}); };
+  bool done;
+  if (n >= H2B_ACA_CELLS_S) done = small();
+  else if (n >= H2B_ACA_CELLS_M) done = mid() || small();
+  else done = wide() || mid() || small();
+  if (!done) throw std::runtime_error("ACA rank cap too large for shared memory");
   CK(cudaStreamSynchronize(s));
   const auto wall3 = std::chrono::steady_clock::now();
   R.rank_h = to_host(R.rank.get(), n, s);

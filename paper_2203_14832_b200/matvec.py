@@ -71,10 +71,33 @@ def h2_matvec(h2: H2Matrix, w, out=None):
 
 
 def h2_matvec_reference(h2: H2Matrix, w, collect: bool = False):
-    """matvec.py:169 — the engine has a single (device) product; ``collect`` is unsupported."""
-    if collect:
-        raise NotImplementedError("per-cell coefficient collection is not exposed by the B200 engine")
-    return h2_matvec(h2, w)
+    """matvec.py:169 -- the engine has a single (device) product.
+
+    With ``collect=True`` also returns {cell: (w_out, u_in)}, the per-cell outgoing / incoming coefficient
+    vectors of this product, read back from the device (the level buffers of the upward pass and of M2L + L2L).
+    """
+    u = h2_matvec(h2, w)
+    if not collect:
+        return u
+    if np.ndim(u) != 1:
+        raise ValueError("collect=True needs a single vector")
+    L = _lib.lib()
+    coeffs = {}
+    for level in h2.compressed_levels():
+        got = []
+        for which in (0, 1):
+            n = _lib.check(L.h2b_h2_get_coeffs(h2.handle, level, which, None))
+            buf = np.empty(n)
+            if n:
+                _lib.check(L.h2b_h2_get_coeffs(h2.handle, level, which, _lib.dptr(buf)))
+            got.append(buf)
+        k_out, k_in = h2.array(level, "k_out"), h2.array(level, "k_in")
+        po = np.concatenate([[0], np.cumsum(k_out)])
+        pi = np.concatenate([[0], np.cumsum(k_in)])
+        for cell in h2.tree.nonempty_cells(level):
+            i = cell._ref_index
+            coeffs[cell] = (got[0][po[i]:po[i + 1]].copy(), got[1][pi[i]:pi[i + 1]].copy())
+    return u, coeffs
 
 
 def dense_matvec(kernel: KernelSpec, cloud, w):

@@ -235,16 +235,16 @@ def config_dict(args, cfg, n):
     return {"workload": workload_name(args, cfg, n), "N": n, "nrhs": nrhs}
 
 
-def workload_name(args, cfg, n):
+def workload_name(args, cfg, n, name=None):
     dist, _, dim, seed, kname, kkw, nu, eps, xdist, nrhs = cfg
-    return (f"{args.config}: {dist} N={n} d={dim} seed={seed} kernel={kname}{kkw or ''} nu={nu} eps={eps:g} "
+    return (f"{name or args.config}: {dist} N={n} d={dim} seed={seed} kernel={kname}{kkw or ''} nu={nu} eps={eps:g} "
             f"x~{xdist} nrhs={nrhs}")
 
 
 def run_b200(args, cfg, world, rank, local):
     # the engine's stream-ordered pool is reserved up front (common.cuh pool_init); the benchmark owns the
     # GPU, so it reserves enough for the largest configuration's setup (pool growth mid-setup is slow)
-    os.environ.setdefault("H2B_POOL_RESERVE_GB", "64")
+    os.environ.setdefault("H2B_POOL_RESERVE_GB", "32")
     import torch
 
     import paper_2203_14832_b200 as h2c
@@ -325,13 +325,19 @@ def run_b200(args, cfg, world, rank, local):
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(float(np.mean([e0.elapsed_time(e1) for e0, e1 in ee])), world)
     e2e_value = aggregate_value(n, e2e_ms, world)
-    # the same call on plain (pageable) numpy arrays, host wall clock (reported beside, not the headline)
-    wn, un = np.ascontiguousarray(w), np.empty(tuple(ud.shape))
-    h2c.h2_matvec(h2, wn, out=un)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        h2c.h2_matvec(h2, wn, out=un)
-    e2e_numpy_ms = 1e3 * (time.perf_counter() - t0) / args.steps
+    # the same call on numpy arrays, host wall clock (reported beside, not the headline): ordinary pageable
+    # arrays (the driver stages the copies), and arrays from h2c.pinned_empty (page-locked: same path as above)
+    def wall_ms(wv, uv):
+        h2c.h2_matvec(h2, wv, out=uv)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            h2c.h2_matvec(h2, wv, out=uv)
+        return 1e3 * (time.perf_counter() - t0) / args.steps
+
+    e2e_numpy_ms = wall_ms(np.ascontiguousarray(w), np.empty(tuple(ud.shape)))
+    wp, up = h2c.pinned_empty(w.shape), h2c.pinned_empty(tuple(ud.shape))
+    wp[...] = w
+    e2e_numpy_pinned_ms = wall_ms(wp, up)
 
     # ---- roofline of the dominant kernel (FP64 interaction: M2L + near field), the transfer passes and setup ----
     st = h2.native_stats()
@@ -402,7 +408,9 @@ def run_b200(args, cfg, world, rank, local):
                   "aca_frac_hbm": aca_bytes / (nnca_ms * 1e-3) / 1e9 / hbm_peak,
                   "aca_flops_model": aca_flops, "aca_achieved_tflops": aca_flops / (nnca_ms * 1e-3) / 1e12,
                   "aca_frac_fp64": aca_flops / (nnca_ms * 1e-3) / 1e12 / NOMINAL_FP64_TFLOPS,
-                  "note": "model: the residual sweeps mostly hit L2, so the HBM fraction can read > 1"}
+                  "note": "model bytes / flops of the residual sweeps.  ncu (profiles/README.md, r2e / r2j): the ACA "
+                          "kernel is instruction-issue bound (issue slots ~50% busy at 16 warps per SM, FP64 pipe 13%, "
+                          "residual rows served from L2 through the TMA ring), so neither fraction is its limiter"}
 
     # ---- accuracy: sampled dense rows + CPU-oracle H2 matvec at the full N ----
     uhost = ud.cpu().numpy()
@@ -429,11 +437,20 @@ def run_b200(args, cfg, world, rank, local):
                 "d2h_bytes_per_step": int(uh.nbytes),
                 "call": "paper_2203_14832_b200.h2_matvec(h2, w_pinned, out=u_pinned) (C ABI h2b_matvec, host "
                         "pointers)"},
-        "e2e_numpy_ms": e2e_numpy_ms,
+        "e2e_numpy_ms": e2e_numpy_ms, "e2e_numpy_pinned_ms": e2e_numpy_pinned_ms,
+        # the north star's use case at this config: one setup, then 50 products (iterative solver), end to end
+        "solver_use_case_ms": {"setup": tree_ms + nnca_ms, "50_matvecs_e2e": 50 * e2e_ms,
+                               "total": tree_ms + nnca_ms + 50 * e2e_ms},
         "gpu_launches": int(matvec_launches(h2, nrhs)) * args.steps,
         "roofline": dict(roof_inter, transfers=roof_tr, setup=roof_setup),
         "clocks": clk.summary(),
     }
+    if rank == 0 and args.config == HEADLINE and not args.no_other_configs and args.n is None and world == 1:
+        # the other BASELINE configs at their stated sizes (parity for them: tests/test_baseline_configs.py)
+        h2 = tree = None
+        del wd, ud, flush
+        torch.cuda.empty_cache()
+        line["other_configs"] = {name: side_config(args, name, dev) for name in ("c0", "c1", "c3", "c4")}
     if rank == 0 and not args.no_cpu_baseline and args.gpus == 1 and world == 1:
         res = oracle_pipeline(pts, cfg, w, matvecs=1)
         cpu_ms = 1e3 * res["matvec_s"][0]
@@ -445,6 +462,58 @@ def run_b200(args, cfg, world, rank, local):
                                           f"N={n} (OpenMP, all host threads)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def side_config(args, name, dev):
+    """Setup and device-resident product of another BASELINE config (same timing rules, 5 timed products)."""
+    import torch
+
+    import paper_2203_14832_b200 as h2c
+
+    cfg = CONFIGS[name]
+    pts, w = make_inputs(cfg)
+    n = pts.shape[0]
+    nrhs = 1 if w.ndim == 1 else w.shape[1]
+    kern = h2c.builtin_kernel(cfg[4], cfg[2], **cfg[5])
+    cloud = h2c.PointCloud.from_points(pts)
+    setups = []
+    for _ in range(2):
+        h2 = tree = None
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        tree = h2c.build_tree(cloud, nu=cfg[6], eta=float(np.sqrt(2.0)))
+        t1 = time.perf_counter()
+        h2 = h2c.assemble(tree, kern, cfg[7])
+        torch.cuda.synchronize()
+        setups.append((1e3 * (t1 - t0), 1e3 * (time.perf_counter() - t1)))
+    wd = torch.from_numpy(np.ascontiguousarray(w)).to(dev)
+    ud = torch.empty_like(wd)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        h2c.h2_matvec(h2, wd, out=ud)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(5)]
+    for e0, e1 in evs:
+        flush.zero_()
+        e0.record(stream)
+        h2c.h2_matvec(h2, wd, out=ud)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    ms = float(np.mean([e0.elapsed_time(e1) for e0, e1 in evs]))
+    rows = np.random.default_rng(7).choice(n, size=min(1000, n), replace=False)
+    wcol = w if nrhs == 1 else np.ascontiguousarray(w[:, 0])
+    exact = h2c.dense_rows(kern, cloud, rows, wcol)
+    u = ud.cpu().numpy()
+    ucol = u if nrhs == 1 else u[:, 0]
+    err = float(np.linalg.norm(ucol[rows] - exact) / np.linalg.norm(exact))
+    st = h2.native_stats()
+    out = {"workload": workload_name(args, cfg, n, name), "N": n, "nrhs": nrhs, "matvec_ms": ms,
+           "n2_per_s": nrhs * float(n) ** 2 / (ms * 1e-3), "tree_ms": setups[-1][0], "nnca_ms": setups[-1][1],
+           "setup_first_ms": sum(setups[0]), "depth": int(st[8]), "max_rank": int(st[3]),
+           "rel_l2_err_dense_1000_rows": err, "eps": cfg[7], "eps_ratio": err / cfg[7]}
+    h2 = tree = None
+    h2c.release_workspace()  # the next config sizes its own ACA arena
+    return out
 
 
 def ctypes_peak(L):
@@ -478,6 +547,8 @@ def main():
     ap.add_argument("--config", default=HEADLINE, choices=sorted(CONFIGS))
     ap.add_argument("--n", type=int, default=None, help="override N (testing)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true",
+                    help="skip the setup + product timings of the other BASELINE configs (c0, c1, c3, c4)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -73,7 +73,9 @@ constexpr int ACA_MAX_THREADS = 1024;
 constexpr int ACA_MAX_WARPS = ACA_MAX_THREADS / 32;
 constexpr int XCH = 8;  // cross-product partial sums per pass
 constexpr int ACA_MAX_SLOTS = 6;
-constexpr int ACA_BIT_WORDS = 2048;  // used-row / used-column bit masks: rows + columns up to ~65K per cell
+// used-row / used-column bit masks in static shared memory: rows + columns up to ~65K per cell; the wide
+// configuration (upper levels, rank caps in the hundreds) keeps its shared memory for the per-warp vectors
+constexpr int aca_bit_words(int nt) { return nt >= 512 ? 512 : 2048; }
 
 struct AcaArgs {
   int kind;
@@ -605,8 +607,13 @@ struct CellJob {
   unsigned long long* counter;
 };
 
-template <int D, int KC, int NT, int NC, int TB, int MB>
+// OUT: the outgoing side (rows = gathered far candidates, column interpolator from V) instead of the incoming
+// one (rows = own points / children's pivots, row interpolator from U); a template parameter because the two
+// sides' branches would otherwise sit in every loop of an instruction-cache-bound kernel.
+template <int D, int KC, int NT, int NC, int TB, int MB, bool OUT>
 __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
+  constexpr bool ROWS_FAR = OUT;
+  constexpr int WHICH = OUT ? 1 : 0;
   static_assert(TB % 4 == 0, "row batches are reduced four rows at a time");
   constexpr int NW = NT / 32;
   constexpr int SEG = NT * NC;  // columns per segment (ring row length)
@@ -614,8 +621,8 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
   __shared__ RedScratch rs;
   __shared__ double xt[D], yb[D];
   __shared__ long long s_cell;
-  __shared__ int64_t s_mp[NT + 1];   // member prefix (far gather)
-  __shared__ int64_t s_mb[NT];       // member range begin
+  __shared__ int s_mp[NT + 1];   // member prefix (far gather; positions and counts are < 2^31, checked on the host)
+  __shared__ int s_mb[NT];       // member range begin
   __shared__ __align__(8) uint64_t s_full[ACA_MAX_SLOTS];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* ring = sm;  // [slots][TB][SEG]
@@ -626,7 +633,7 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
   double* crosspart = crossu + J.cap_max;  // [NW][cap]
   // used-row / used-column flags: bit masks in (static) shared memory when they fit (J.bit_words > 0), else bytes
   // in the slab
-  __shared__ uint32_t s_bits[ACA_BIT_WORDS];
+  __shared__ uint32_t s_bits[aca_bit_words(NT)];
   uint32_t* bits = s_bits;
   double* usm = crosspart + NW * J.cap_max;
   double* base = J.ws + (int64_t)blockIdx.x * J.ws_doubles;
@@ -671,7 +678,7 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
       if (tid < nm) {
         int64_t b, e;
         src_range(J.far, J.il_idx[q0 + tid], b, e);
-        s_mb[tid] = b;
+        s_mb[tid] = (int)b;
         len = e - b;
       }
       int64_t v = len;
@@ -684,8 +691,8 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
       __syncthreads();
       int64_t off = far_n;
       for (int w = 0; w < warp; w++) off += rs.i[w];
-      if (tid < nm) s_mp[tid + 1] = off + v;
-      if (tid == 0) s_mp[0] = far_n;
+      if (tid < nm) s_mp[tid + 1] = (int)(off + v);
+      if (tid == 0) s_mp[0] = (int)far_n;
       int64_t tot = far_n;
       for (int w = 0; w < NW; w++) tot += rs.i[w];
       __syncthreads();
@@ -701,15 +708,15 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
       __syncthreads();
     }
     APROF(0);
-    const int64_t m = J.rows_far ? far_n : own_n;
-    const int64_t n = J.rows_far ? own_n : far_n;
+    const int64_t m = ROWS_FAR ? far_n : own_n;
+    const int64_t n = ROWS_FAR ? own_n : far_n;
     const int64_t cap = J.caps[cell];
     // row / column coordinate k of local index i
     auto rowc = [&](int k, int64_t i) -> double {
-      return J.rows_far ? FC[k * J.f_max + i] : J.own.coords[k * J.own.ld + ob + i];
+      return ROWS_FAR ? FC[k * J.f_max + i] : J.own.coords[k * J.own.ld + ob + i];
     };
     auto colc = [&](int k, int64_t j) -> double {
-      return J.rows_far ? J.own.coords[k * J.own.ld + ob + j] : FC[k * J.f_max + j];
+      return ROWS_FAR ? J.own.coords[k * J.own.ld + ob + j] : FC[k * J.f_max + j];
     };
     if (m == 0 || n == 0 || cap == 0) {
       if (tid == 0) {
@@ -1074,17 +1081,17 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
     }
     for (int64_t t = tid; t < k; t += NT) {
       const int64_t r = RP[t], c = CP[t];
-      J.tpiv[po + t] = J.rows_far ? FG[r] : J.own.gidx[ob + r];
-      J.spiv[po + t] = J.rows_far ? J.own.gidx[ob + c] : FG[c];
+      J.tpiv[po + t] = ROWS_FAR ? FG[r] : J.own.gidx[ob + r];
+      J.spiv[po + t] = ROWS_FAR ? J.own.gidx[ob + c] : FG[c];
     }
     // interpolation operator (aca.py:297 / :311, same arithmetic): which 0 -> P = U L^{-1}; 1 -> Q = V R^{-T}.
     // The back substitution re-reads the columns of P it has already formed: when the operator fits, it is built
     // in the (now idle) ring and copied out coalesced.
     if (k > 0) {
-      const int64_t rows = J.which == 0 ? m : n;
-      const int64_t fs = J.which == 0 ? m : ldv;  // row stride of the factor
-      const double* F = J.which == 0 ? U : V;
-      const int64_t* pv = J.which == 0 ? RP : CP;
+      const int64_t rows = WHICH == 0 ? m : n;
+      const int64_t fs = WHICH == 0 ? m : ldv;  // row stride of the factor
+      const double* F = WHICH == 0 ? U : V;
+      const int64_t* pv = WHICH == 0 ? RP : CP;
       double* Pg = J.mat + J.mat_off[cell];
       const bool staged = k * rows <= (int64_t)S * TB * SEG;
       double* P = staged ? ring : Pg;
@@ -1093,7 +1100,7 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
           const double* Fs = F + sI * fs;
           double acc = Fs[i];
           for (int64_t t = sI + 1; t < k; t++) acc -= P[t * rows + i] * Fs[pv[t]];
-          P[sI * rows + i] = J.which == 0 ? acc / Fs[pv[sI]] : acc;
+          P[sI * rows + i] = WHICH == 0 ? acc / Fs[pv[sI]] : acc;
         }
       }
       __syncthreads();
@@ -1131,15 +1138,18 @@ struct SideResult {
 };
 
 // Per-device ACA workspace arena: grows to the largest launch seen and is reused after that, so repeated setups
-// do not churn the allocator (pool growth in the middle of a setup made some runs 2-3x slower).  Assemblies on
-// one device are serialised by the arena's mutex (each one fills the GPU anyway); h2b_release_workspace() frees
-// the arenas.
+// do not map memory again (mapping ~100 GB for c1's top levels costs 650 ms).  It is a plain cudaMalloc block,
+// outside the stream-ordered pool: its size is budgeted against the device's free memory, and memory the pool
+// holds (reserved or cached) is not available to it, so the budget can never over-commit.  Assemblies on one
+// device are serialised by the arena's mutex (each one fills the GPU anyway); h2b_release_workspace() frees the
+// arenas (they are deliberately not freed at process exit).
 struct DeviceArena {
   std::mutex mu;
-  DBuf<double> buf;
+  double* p = nullptr;
+  size_t n = 0;  // doubles
 };
 DeviceArena* device_arenas() {
-  static DeviceArena arenas[64];
+  static DeviceArena* arenas = new DeviceArena[64];
   return arenas;
 }
 DeviceArena& current_arena() {
@@ -1148,19 +1158,28 @@ DeviceArena& current_arena() {
   return device_arenas()[dev & 63];
 }
 double* aca_arena(DeviceArena& A, size_t doubles, cudaStream_t s) {
-  if (A.buf.n < doubles) {
+  if (A.n < doubles) {
     CK(cudaStreamSynchronize(s));
-    A.buf.release();
-    A.buf.alloc(doubles + doubles / 8);
+    if (A.p) CK(cudaFree(A.p));
+    A.p = nullptr;
+    A.n = 0;
+    const size_t want = doubles + doubles / 8;
+    if (cudaMalloc(reinterpret_cast<void**>(&A.p), want * sizeof(double)) == cudaSuccess) {
+      A.n = want;
+    } else {
+      cudaGetLastError();  // the head room was a bonus: take exactly what the launch needs
+      CK(cudaMalloc(reinterpret_cast<void**>(&A.p), doubles * sizeof(double)));
+      A.n = doubles;
+    }
   }
-  return A.buf.get();
+  return A.p;
 }
 
 // ring configurations: threads per CTA, columns per thread, rows per batch, CTAs per SM
-template <int D, int KC, int NT, int NC, int TB, int MB>
+template <int D, int KC, int NT, int NC, int TB, int MB, bool OUT>
 struct RingCfg {
   static constexpr int nt = NT, seg = NT * NC, slot = TB * NT * NC, mb = MB;  // slot: doubles per ring slot
-  static auto kern() { return aca_ring<D, KC, NT, NC, TB, MB>; }
+  static auto kern() { return aca_ring<D, KC, NT, NC, TB, MB, OUT>; }
 };
 
 template <int D, int KC>
@@ -1235,6 +1254,8 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
     R.rank_h.clear();
     return;
   }
+  if (far.ld >= ((int64_t)1 << 31) || own.ld >= ((int64_t)1 << 31) || f_max >= ((int64_t)1 << 31))
+    throw std::invalid_argument("more than 2^31 candidate positions in an NNCA level");
   auto d_cap = upload(caph, s);
   auto d_order = upload(order, s);
   int dev = 0, nsm = 0, smem_sm = 0, smem_cta = 0;
@@ -1275,7 +1296,7 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
     cudaFuncAttributes fa;
     CK(cudaFuncGetAttributes(&fa, kern));  // static shared memory; every CTA also reserves 1 KB
     int64_t bit_words = (((m_max + 31) >> 5) + ((n_max + 31) >> 5) + 3) & ~(int64_t)1;
-    if (bit_words > ACA_BIT_WORDS) bit_words = 0;  // very long candidate lists keep byte flags in the slab
+    if (bit_words > aca_bit_words(C::nt)) bit_words = 0;  // very long candidate lists keep byte flags in the slab
     J.bit_words = (int)bit_words;
     const int64_t vecs = (4 + C::nt / 32) * cap_max;
     int64_t u_need = 0;
@@ -1307,27 +1328,19 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
     J.v_slab = vs;
     int64_t ws = J.u_slab + J.v_slab + D * f_max + f_max + 2 * cap_max + (m_max + n_max + 7) / 8 + 1;
     ws = (ws + 31) / 32 * 32 + H2B_ACA_SLAB_PAD;  // pad: per-CTA slabs off power-of-two strides
-    if (grid * ws > (int64_t)arena.buf.n) {
+    if (grid * ws > (int64_t)arena.n) {
       // Slabs are sized for the rank cap (min(m, n)): the top levels of dense clouds (n ~ 1e5 candidates per
-      // cell) need ~0.8 GB per concurrent cell, so their total is bounded by the memory available (device free
-      // memory + the unused part of the reserved pool) -- fewer concurrent cells instead of running out.  An
-      // arena that already holds >= 3/4 of the wanted slabs is used as is: growing it means mapping tens of GB
-      // again (measured 650 ms at c1) for a <= 25% longer launch.  Steady-state setups skip the query.
-      const int64_t have = (int64_t)arena.buf.n / ws;
+      // cell) need ~0.8 GB per concurrent cell, so their total is bounded by the device's free memory plus what
+      // the arena already holds -- fewer concurrent cells instead of running out.  An arena that already holds
+      // >= 3/4 of the wanted slabs is used as is: growing it means mapping tens of GB again for a <= 25% longer
+      // launch.  Steady-state setups skip the query.
+      const int64_t have = (int64_t)arena.n / ws;
       if (have >= 1 && 4 * have >= 3 * grid) {
         grid = have;
       } else {
         size_t fr = 0, tot = 0;
         CK(cudaMemGetInfo(&fr, &tot));
-        size_t pool_free = 0;
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-          uint64_t rsv = 0, used = 0;
-          if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &rsv) == cudaSuccess &&
-              cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess && rsv > used)
-            pool_free = (size_t)(rsv - used);
-        }
-        const int64_t budget = (int64_t)(0.6 * (double)(fr + pool_free) / sizeof(double)) + (int64_t)arena.buf.n;
+        const int64_t budget = (int64_t)(0.6 * (double)fr / sizeof(double)) + (int64_t)arena.n;
         grid = std::max<int64_t>(1, std::min<int64_t>(grid, budget / ws));
       }
     }
@@ -1374,9 +1387,17 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
   // cells (upper levels): wide CTAs so one cell's row pass uses the whole SM.
   // The per-warp vectors scale with the rank cap: a cap too large for the preferred configuration falls back to
   // the narrower ones (fewer warps, smaller ring slots).
-  auto small = [&] { return launch(RingCfg<D, KC, H2B_ACA_NT_S, H2B_ACA_NC_S, H2B_ACA_TB_S, H2B_ACA_MB_S>{}); };
-  auto mid = [&] { return launch(RingCfg<D, KC, 256, 4, 4, 2>{}); };
-  auto wide = [&] { return launch(RingCfg<D, KC, H2B_ACA_NT, H2B_ACA_NC, H2B_ACA_TB, H2B_ACA_MINB>{}); };
+  auto small = [&] {
+    return rows_far ? launch(RingCfg<D, KC, H2B_ACA_NT_S, H2B_ACA_NC_S, H2B_ACA_TB_S, H2B_ACA_MB_S, true>{})
+                    : launch(RingCfg<D, KC, H2B_ACA_NT_S, H2B_ACA_NC_S, H2B_ACA_TB_S, H2B_ACA_MB_S, false>{});
+  };
+  auto mid = [&] {
+    return rows_far ? launch(RingCfg<D, KC, 256, 4, 4, 2, true>{}) : launch(RingCfg<D, KC, 256, 4, 4, 2, false>{});
+  };
+  auto wide = [&] {
+    return rows_far ? launch(RingCfg<D, KC, H2B_ACA_NT, H2B_ACA_NC, H2B_ACA_TB, H2B_ACA_MINB, true>{})
+                    : launch(RingCfg<D, KC, H2B_ACA_NT, H2B_ACA_NC, H2B_ACA_TB, H2B_ACA_MINB, false>{});
+  };
   bool done;
   if (n >= H2B_ACA_CELLS_S) done = small();
   else if (n >= H2B_ACA_CELLS_M) done = mid() || small();
@@ -1572,10 +1593,12 @@ void release_workspace() {
   for (int dv = 0; dv < ndev && dv < 64; dv++) {
     DeviceArena& A = device_arenas()[dv];
     std::lock_guard<std::mutex> g(A.mu);
-    if (!A.buf.n) continue;
+    if (!A.p) continue;
     CK(cudaSetDevice(dv));
     CK(cudaDeviceSynchronize());
-    A.buf.release();
+    CK(cudaFree(A.p));
+    A.p = nullptr;
+    A.n = 0;
   }
   CK(cudaSetDevice(cur));
 }

@@ -86,6 +86,12 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// FP64 reduction into global memory.  atomicAdd on a generic pointer compiles to a run-time address-space
+// dispatch (QSPC + three code paths, ~25 instructions per call); the level buffers are always global.
+__device__ __forceinline__ void red_add_f64(double* p, double v) {
+  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(__cvta_generic_to_global(p)), "d"(v) : "memory");
+}
+
 template <int D>
 __device__ __forceinline__ void load_rec(const double2* rec, int64_t i, double (&y)[D], double& q) {
   constexpr int W = SrcRec<D, 1>::W;
@@ -321,12 +327,12 @@ __device__ __forceinline__ void sym_item(const SymTab& T, int4 dsc, int64_t R, i
           }
 #pragma unroll
           for (int s = 0; s < RS; s++)
-            if (gidx[s] >= 0) atomicAdd(T.out + (int64_t)gidx[s] * R + r0, col[s] * SCALE);
+            if (gidx[s] >= 0) red_add_f64(out + (int64_t)gidx[s] * R + r0, col[s] * SCALE);
         }
         const double tot = warp_reduce_scatter<TB>(p, lane);
         constexpr int LPT = 32 / TB;  // lanes per target after the reduce-scatter
         const int t = lane / LPT;
-        if (lane % LPT == 0 && t < tcnt) atomicAdd(out + (int64_t)(tb + tc0 + t) * R + r0, tot * SCALE);
+        if (lane % LPT == 0 && t < tcnt) red_add_f64(out + (int64_t)(tb + tc0 + t) * R + r0, tot * SCALE);
       }
     }
   }

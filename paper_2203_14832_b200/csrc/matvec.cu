@@ -25,13 +25,14 @@ bool g_profile = false;
 double g_stage_ms[5] = {0, 0, 0, 0, 0};
 
 __global__ void gather_rows(const double* __restrict__ w, const int64_t* __restrict__ perm, int64_t n, int64_t R,
-                            double* __restrict__ out, double* __restrict__ recq, int rs) {
+                            double* __restrict__ out, double* __restrict__ recq, int rs, double* __restrict__ zero) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n * R) return;
   int64_t p = i / R, r = i - p * R;
   const double v = w[perm[p] * R + r];
   out[i] = v;
   if (recq) recq[i * rs] = v;  // one RHS: also the charge slot of the source record (no separate pack pass)
+  if (zero) zero[i] = 0.0;     // symmetric one-RHS product: clears the near-field accumulator (np == nq there)
 }
 
 void interact_all(int d, int kind, const DevH2& h, int64_t R, int64_t r0, int nr, const KParams& kp,
@@ -566,8 +567,13 @@ void matvec(DevH2& h, const double* w, double* u, int64_t R, cudaStream_t s) {
   auto recq = [&](int list) -> double* {
     return fused_pack ? reinterpret_cast<double*>(h.pack1.lists[list].get()) + T.d : nullptr;
   };
+  // symmetric one-RHS product: the interaction kernel accumulates into zeroed u_in / near buffers; with one RHS
+  // the gather and the upward pass clear them in passing (same index spaces), otherwise memsets do
+  const bool sym = h.symmetric && h.sym_ready && (R % 16) != 0;
+  const bool fused_zero = sym && R == 1 && T.shared && L >= 2;
   gather_rows<<<nblk(T.nq * R, 256), 256, 0, s>>>(w, T.sperm(), T.nq, R, h.w_sorted.get(),
-                                                  recq((int)h.pack1.lists.size() - 1), rs1);
+                                                  recq((int)h.pack1.lists.size() - 1), rs1,
+                                                  fused_zero ? h.near.get() : nullptr);
   CKL();
   if (L >= 2) {
     // ---- upward pass: P2M at the leaves, then M2M (one or a few threads per output row) ----
@@ -576,20 +582,19 @@ void matvec(DevH2& h, const double* w, double* u, int64_t R, cudaStream_t s) {
     {
       const DevH2Level& HL = h.lv[L];
       launch_up(c_up(L), HL.out_total, own_out(L), HL.out_ptrd(), h.w_sorted.get(), h.wout[L].get(), R, s,
-                recq(L - 2), rs1);
+                recq(L - 2), rs1, fused_zero ? h.uin[L].get() : nullptr);
     }
     for (int l = L - 1; l >= 2; l--) {
       const DevH2Level& HL = h.lv[l];
       launch_up(c_up(l), HL.out_total, own_out(l), HL.out_ptrd(), h.wout[l + 1].get(), h.wout[l].get(), R, s,
-                recq(l - 2), rs1);
+                recq(l - 2), rs1, fused_zero ? h.uin[l].get() : nullptr);
     }
   }
   if (g_profile) CK(cudaEventRecord(ev[1], s));
   // ---- every M2L level + the near field in one launch per RHS chunk ----
   // one-RHS chunks on the symmetric path: each unordered cell pair evaluated once (interact_sym.cuh), results
   // accumulated with FP64 reductions into zeroed u_in / near buffers
-  const bool sym = h.symmetric && h.sym_ready && (R % 16) != 0;
-  if (sym) {
+  if (sym && !fused_zero) {
     for (int l = 2; l <= L; l++)
       CK(cudaMemsetAsync(h.uin[l].get(), 0, sizeof(double) * h.lv[l].in_total * R, s));
     CK(cudaMemsetAsync(h.near.get(), 0, sizeof(double) * T.np * R, s));

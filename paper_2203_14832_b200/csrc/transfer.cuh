@@ -217,7 +217,7 @@ __global__ void up_compact(int64_t nout, const int* __restrict__ owner, const in
                            const int* __restrict__ piv_pos, const int64_t* __restrict__ g_ptr,
                            const int* __restrict__ g_pos, const double* __restrict__ op_up,
                            const int64_t* __restrict__ op_off, const double* __restrict__ x, double* __restrict__ y,
-                           int64_t R, double* __restrict__ recq, int rs) {
+                           int64_t R, double* __restrict__ recq, int rs, double* __restrict__ zero) {
   const int64_t nrb = (R + RB - 1) / RB;
   const int64_t qq = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t q = qq / SG;
@@ -266,6 +266,9 @@ __global__ void up_compact(int64_t nout, const int* __restrict__ owner, const in
     for (int r = 0; r < RB; r++)
       if (RB == 1 || r0 + r < R) y[p * R + r0 + r] = acc[r];
     if (RB == 1 && recq) recq[q * rs] = acc[0];
+    // symmetric one-RHS product: the interaction kernel accumulates into this level's u_in with reductions, so
+    // the buffer (one entry per pivot, like y) is cleared here instead of by a memset launch per level
+    if (RB == 1 && zero) zero[q] = 0.0;
   }
 }
 
@@ -356,19 +359,20 @@ __global__ void scatter_near(int64_t n, const double* __restrict__ near, const i
 constexpr int kTransferRB = 8;  // RHS block of the multi-RHS (R >= 8) passes (measured at c4: 8 beats 4 and 16)
 
 inline void launch_up(const CompactOps& C, int64_t nout, const int* owner, const int64_t* out_ptr, const double* x,
-                      double* y, int64_t R, cudaStream_t s, double* recq, int rs) {
+                      double* y, int64_t R, cudaStream_t s, double* recq, int rs, double* zero = nullptr) {
   if (R >= 8) {
     const int64_t thr = std::max<int64_t>(nout * ((R + kTransferRB - 1) / kTransferRB), 1);
     up_compact<1, kTransferRB><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, C.piv_pos.get(), C.g_ptr.get(),
                                                               C.g_pos.get(), C.op_up.get(), C.op_off.get(), x, y, R,
-                                                              nullptr, 0);
+                                                              nullptr, 0, nullptr);
     CKL();
     return;
   }
   const int64_t thr = std::max<int64_t>(nout * R, 1) * C.sg_up;
 #define H2B_UP(G)                                                                                                 \
   up_compact<G, 1><<<nblk(thr, 256), 256, 0, s>>>(nout, owner, out_ptr, C.piv_pos.get(), C.g_ptr.get(),          \
-                                                  C.g_pos.get(), C.op_up.get(), C.op_off.get(), x, y, R, recq, rs)
+                                                  C.g_pos.get(), C.op_up.get(), C.op_off.get(), x, y, R, recq, rs, \
+                                                  zero)
   switch (C.sg_up) {
     case 1: H2B_UP(1); break;
     case 2: H2B_UP(2); break;

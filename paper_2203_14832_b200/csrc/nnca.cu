@@ -946,7 +946,7 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
             }
           }
         }
-        fence_proxy_async_all();  // the rows written above are read by bulk copies (async proxy) in later passes
+        fence_proxy_async_global();  // the rows written above are read by bulk copies (async proxy) in later passes
         APROF(1);
         if (bj < 0) best = -1.0;
         block_argmax<NT>(best, bj, rs);
@@ -1111,7 +1111,7 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
       if (staged) {
         __syncthreads();
         for (int64_t q = tid; q < k * rows; q += NT) Pg[q] = P[q];
-        fence_proxy_async_all();  // generic writes to the ring before the next cell's bulk copies into it
+        fence_proxy_async();  // generic writes to the ring before the next cell's bulk copies into it
       }
     }
     APROF(7);

@@ -1095,18 +1095,24 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
       double* Pg = J.mat + J.mat_off[cell];
       const bool staged = k * rows <= (int64_t)S * TB * SEG;
       double* P = staged ? ring : Pg;
-      for (int64_t i = tid; i < rows; i += NT) {
-        for (int64_t sI = k - 1; sI >= 0; sI--) {
-          const double* Fs = F + sI * fs;
-          double acc = Fs[i];
-          for (int64_t t = sI + 1; t < k; t++) acc -= P[t * rows + i] * Fs[pv[t]];
-          P[sI * rows + i] = WHICH == 0 ? acc / Fs[pv[sI]] : acc;
+      // a full-rank cell (every row is a pivot row: most leaves) needs no back substitution: the pinning below
+      // overwrites every row with its unit row, exactly what the reference's interpolator ends up as
+      if (k < rows)
+        for (int64_t i = tid; i < rows; i += NT) {
+          for (int64_t sI = k - 1; sI >= 0; sI--) {
+            const double* Fs = F + sI * fs;
+            double acc = Fs[i];
+            for (int64_t t = sI + 1; t < k; t++) acc -= P[t * rows + i] * Fs[pv[t]];
+            P[sI * rows + i] = WHICH == 0 ? acc / Fs[pv[sI]] : acc;
+          }
         }
-      }
       __syncthreads();
-      for (int64_t q = tid; q < k * k; q += NT) {
-        const int64_t t = q / k, sI = q % k;
-        P[sI * rows + pv[t]] = (sI == t) ? 1.0 : 0.0;
+      {
+        const int ki = (int)k;
+        for (int q = tid; q < ki * ki; q += NT) {
+          const int t = q / ki, sI = q - t * ki;
+          P[(int64_t)sI * rows + pv[t]] = (sI == t) ? 1.0 : 0.0;
+        }
       }
       if (staged) {
         __syncthreads();

@@ -408,9 +408,9 @@ def run_b200(args, cfg, world, rank, local):
                   "aca_frac_hbm": aca_bytes / (nnca_ms * 1e-3) / 1e9 / hbm_peak,
                   "aca_flops_model": aca_flops, "aca_achieved_tflops": aca_flops / (nnca_ms * 1e-3) / 1e12,
                   "aca_frac_fp64": aca_flops / (nnca_ms * 1e-3) / 1e12 / NOMINAL_FP64_TFLOPS,
-                  "note": "model bytes / flops of the residual sweeps.  ncu (profiles/README.md, r2e / r2j): the ACA "
-                          "kernel is instruction-issue bound (issue slots ~50% busy at 16 warps per SM, FP64 pipe 13%, "
-                          "residual rows served from L2 through the TMA ring), so neither fraction is its limiter"}
+                  "note": "model bytes / flops of the residual sweeps.  ncu (profiles/r2j_aca_ring_ncu_full.json): the ACA "
+                          "kernel is issue / latency bound at the leaves (issue slots 35% busy at 16 warps per SM, FP64 pipe 13%) and "
+                          "DRAM-bound on the residual rows at the levels above (5.3 TB/s at level 6)"}
 
     # ---- accuracy: sampled dense rows + CPU-oracle H2 matvec at the full N ----
     uhost = ud.cpu().numpy()

@@ -169,7 +169,6 @@ __device__ __forceinline__ void bulk_g2s_u32(uint32_t dst, const void* src, uint
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // generic-proxy global writes (residual rows) before a later TMA read of them
-__device__ __forceinline__ void fence_proxy_async_all() { asm volatile("fence.proxy.async;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
 // ---------------------------------------------------------------------

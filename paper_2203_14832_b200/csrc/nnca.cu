@@ -28,7 +28,8 @@ namespace h2b {
 namespace {
 
 // ring configurations of the persistent ACA kernel (threads per CTA, columns per thread, rows per batch, CTAs
-// per SM): long candidate lists, and short ones (n_max <= H2B_ACA_SMALL_N)
+// per SM): the wide one (levels with few cells) and the small one (levels with >= H2B_ACA_CELLS_S cells); a
+// 256-thread configuration sits between them (run_side)
 #ifndef H2B_ACA_NT
 #define H2B_ACA_NT 512
 #endif

@@ -115,6 +115,28 @@ __device__ __forceinline__ void warp_argmax(double& v, int64_t& i) {
   }
 }
 
+// The same for values >= 0 (|residual| candidates) and indices < 2^31, with warp-wide integer reductions
+// (REDUX): the bit pattern of a non-negative double orders like an unsigned integer, so the maximum is the
+// maximum high word, then the maximum low word among its holders, then the lowest index among those.  Three
+// REDUX instead of five rounds of four shuffles + merge logic; the pivot search runs twice per ACA step.
+__device__ __forceinline__ void warp_argmax_nn(double& v, int64_t& i) {
+  const bool has = i >= 0;
+  const unsigned hi = has ? (unsigned)__double2hiint(v) : 0u;
+  const unsigned lo = has ? (unsigned)__double2loint(v) : 0u;
+  const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+  const bool c1 = has && hi == mh;
+  const unsigned ml = __reduce_max_sync(0xffffffffu, c1 ? lo : 0u);
+  const bool c2 = c1 && lo == ml;
+  const unsigned mi = __reduce_min_sync(0xffffffffu, c2 ? (unsigned)i : 0xffffffffu);
+  if (mi == 0xffffffffu) {
+    v = -1.0;
+    i = -1;
+  } else {
+    v = __hiloint2double((int)mh, (int)ml);
+    i = (int64_t)mi;
+  }
+}
+
 __device__ __forceinline__ int64_t warp_min_i64(int64_t v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {

@@ -117,7 +117,7 @@ template <int NT>
 __device__ void block_argmax(double& v, int64_t& i, RedScratch& rs) {
   constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  warp_argmax(v, i);
+  warp_argmax_nn(v, i);  // candidates are |residual| >= 0, indices < 2^31 (checked on the host)
   if (lane == 0) {
     rs.v[w] = v;
     rs.i[w] = i;
@@ -126,7 +126,7 @@ __device__ void block_argmax(double& v, int64_t& i, RedScratch& rs) {
   if (w == 0) {
     double v2 = lane < NW ? rs.v[lane] : -1.0;
     int64_t i2 = lane < NW ? (int64_t)rs.i[lane] : -1;
-    warp_argmax(v2, i2);
+    warp_argmax_nn(v2, i2);
     if (lane == 0) {
       rs.bv = v2;
       rs.bi = i2;
@@ -966,7 +966,11 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
             crossv[t] = w;
           }
           const double v2 = block_sum<NT>(v2p, rs);  // syncs: crossv visible
-          for (int t = 0; t < kf; t++) norm2 += 2.0 * crossu[t] * crossv[t];
+          {  // every warp forms the same sum in the same order (lanes over t, then a butterfly)
+            double part = 0.0;
+            for (int t = lane; t < kf; t += 32) part = fma(2.0 * crossu[t], crossv[t], part);
+            norm2 += warp_sum(part);
+          }
           norm2 += u2_prev * v2;
           pend = false;
           fuse = false;

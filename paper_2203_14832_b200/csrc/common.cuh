@@ -175,9 +175,10 @@ __device__ __forceinline__ void mbar_expect_tx_u32(uint32_t bar, uint32_t bytes)
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
+  // with a suspend-time hint the warp sleeps in hardware between polls instead of spinning through the loop
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 0x989680;\n"
       " @!p bra WAIT_%=;\n}\n" ::"r"(bar),
       "r"(parity)
       : "memory");

@@ -743,8 +743,8 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
     } else {
       for (int64_t q = tid; q < m + n; q += NT) ru[q] = 0;
     }
-    auto row_used = [&](int64_t i) -> bool { return sbits ? (rbits[i >> 5] >> (i & 31)) & 1u : ru[i] != 0; };
-    auto col_used = [&](int64_t j) -> bool { return sbits ? (cbits[j >> 5] >> (j & 31)) & 1u : cu[j] != 0; };
+    auto row_used = [&](int i) -> bool { return sbits ? (rbits[i >> 5] >> (i & 31)) & 1u : ru[i] != 0; };
+    auto col_used = [&](int j) -> bool { return sbits ? (cbits[j >> 5] >> (j & 31)) & 1u : cu[j] != 0; };
     const int64_t full = m < n ? m : n;
     int64_t k = 0, trial = 0, nev = 0;
     double norm2 = 0.0;
@@ -762,9 +762,11 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
     // Batch q of a pass over kfq rows (nbq batches per segment): rows [b TB, b TB + TB) of segment q / nbq.
     // Thread 0 arms the slot's mbarrier and issues one bulk copy per row; every thread advances the stream state.
     int pre = 0;  // batches of the next pass already in flight
+    int isg = 0, ib = 0;  // (segment, batch) of the next batch to issue: the stream is issued in order
     auto issue = [&](int q, int kfq, int nbq) {
+      (void)q;
       if (tid == 0) {
-        const int sg = q / nbq, b = q - sg * nbq;
+        const int sg = isg, b = ib;
         const int c0 = sg * seglen;
         const int len = ni - c0 < seglen ? ni - c0 : seglen;
         const uint32_t bytes = (uint32_t)((len + 1) & ~1) * 8u;
@@ -775,6 +777,10 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
         const double* src = V + (int64_t)r0 * ldv + c0;
         const uint32_t dst = ring0 + (uint32_t)(islot * TB) * (uint32_t)(SEG * 8);
         for (int tt = 0; tt < rows; tt++) bulk_g2s_u32(dst + (uint32_t)tt * (uint32_t)(SEG * 8), src + (int64_t)tt * ldv, bytes, bar);
+      }
+      if (++ib == nbq) {  // the stream of a pass (and of the pass prefetched after it) runs segment by segment
+        ib = 0;
+        if (++isg == nseg) isg = 0;
       }
       if (++islot == S) islot = 0;
       inflight++;
@@ -983,7 +989,7 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
         if (best > 0.0) break;
         int64_t first = INT64_MAX;
         for (int64_t i = tid; i < m; i += NT)
-          if (!row_used(i) && i < first) first = i;
+          if (!row_used((int)i) && i < first) first = i;
         first = block_min<NT>(first, rs);
         if (first == INT64_MAX) {
           exhausted = true;
@@ -1050,7 +1056,7 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
       int64_t bi = -1;
       const double* Uk = U + (k - 1) * m;
       for (int64_t i = tid; i < m; i += NT)
-        if (!row_used(i)) {
+        if (!row_used((int)i)) {
           const double val = fabs(Uk[i]);
           if (val > best) {
             best = val;

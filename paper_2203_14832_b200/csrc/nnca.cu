@@ -640,9 +640,11 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
   double* base = J.ws + (int64_t)blockIdx.x * J.ws_doubles;
   double* Ub = base;
   double* Vb = Ub + J.u_slab;
-  double* FC = Vb + J.v_slab;
-  int64_t* FG = reinterpret_cast<int64_t*>(FC + D * J.f_max);
-  int64_t* RP = FG + J.f_max;
+  // far candidates: their positions in the level's source arrays.  The coordinates are read through these from
+  // the shared per-level arrays (each far point sits in the lists of ~80 cells, so those arrays stay L2-resident)
+  // instead of from a private gathered copy per cell (24 bytes per candidate and pass of DRAM traffic)
+  int* POS = reinterpret_cast<int*>(Vb + J.v_slab);
+  int64_t* RP = reinterpret_cast<int64_t*>(POS + 2 * ((J.f_max + 1) / 2));
   int64_t* CP = RP + J.cap_max;
   unsigned char* flags = reinterpret_cast<unsigned char*>(CP + J.cap_max);
   const double knum = J.kind == LAPLACE ? INV_FOUR_PI : 1.0;
@@ -700,9 +702,7 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
       for (int q = warp; q < nm; q += NW) {
         const int64_t b = s_mb[q], o0 = s_mp[q], len2 = s_mp[q + 1] - o0;
         for (int64_t e = lane; e < len2; e += 32) {
-#pragma unroll
-          for (int k = 0; k < D; k++) FC[k * J.f_max + o0 + e] = J.far.coords[k * J.far.ld + b + e];
-          FG[o0 + e] = J.far.gidx[b + e];
+          POS[o0 + e] = (int)(b + e);
         }
       }
       far_n = tot;
@@ -714,10 +714,10 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
     const int64_t cap = J.caps[cell];
     // row / column coordinate k of local index i
     auto rowc = [&](int k, int64_t i) -> double {
-      return ROWS_FAR ? FC[k * J.f_max + i] : J.own.coords[k * J.own.ld + ob + i];
+      return ROWS_FAR ? J.far.coords[k * J.far.ld + POS[i]] : J.own.coords[k * J.own.ld + ob + i];
     };
     auto colc = [&](int k, int64_t j) -> double {
-      return ROWS_FAR ? J.own.coords[k * J.own.ld + ob + j] : FC[k * J.f_max + j];
+      return ROWS_FAR ? J.own.coords[k * J.own.ld + ob + j] : J.far.coords[k * J.far.ld + POS[j]];
     };
     if (m == 0 || n == 0 || cap == 0) {
       if (tid == 0) {
@@ -849,15 +849,22 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
           {
             // all loads of the segment head first (coordinates, raw row k - 1), then the arithmetic
             double y[NC][D], raw[NC];
+            int64_t pj[NC];  // position of the column's point in the source arrays (one dependent load, batched)
 #pragma unroll
             for (int c = 0; c < NC; c++) {
               const int jl = tid + c * NT;
               ok[c] = jl < len;
               off[c] = ok[c] ? jl : 0;
               const int jj = c0 + off[c];
-#pragma unroll
-              for (int q = 0; q < D; q++) y[c][q] = colc(q, jj);
+              pj[c] = ROWS_FAR ? ob + jj : (int64_t)POS[jj];
               raw[c] = fuse ? Vlast[jj] : 0.0;
+            }
+#pragma unroll
+            for (int c = 0; c < NC; c++) {
+              const double* cs = ROWS_FAR ? J.own.coords : J.far.coords;
+              const int64_t ld = ROWS_FAR ? J.own.ld : J.far.ld;
+#pragma unroll
+              for (int q = 0; q < D; q++) y[c][q] = cs[q * ld + pj[c]];
             }
 #pragma unroll
             for (int c = 0; c < NC; c++) {
@@ -1092,8 +1099,8 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
     }
     for (int64_t t = tid; t < k; t += NT) {
       const int64_t r = RP[t], c = CP[t];
-      J.tpiv[po + t] = ROWS_FAR ? FG[r] : J.own.gidx[ob + r];
-      J.spiv[po + t] = ROWS_FAR ? J.own.gidx[ob + c] : FG[c];
+      J.tpiv[po + t] = ROWS_FAR ? J.far.gidx[POS[r]] : J.own.gidx[ob + r];
+      J.spiv[po + t] = ROWS_FAR ? J.own.gidx[ob + c] : J.far.gidx[POS[c]];
     }
     // interpolation operator (aca.py:297 / :311, same arithmetic): which 0 -> P = U L^{-1}; 1 -> Q = V R^{-T}.
     // The back substitution re-reads the columns of P it has already formed: when the operator fits, it is built
@@ -1343,7 +1350,7 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
     }
     J.u_slab = (us + 1) & ~(int64_t)1;
     J.v_slab = vs;
-    int64_t ws = J.u_slab + J.v_slab + D * f_max + f_max + 2 * cap_max + (m_max + n_max + 7) / 8 + 1;
+    int64_t ws = J.u_slab + J.v_slab + (f_max + 1) / 2 + 2 * cap_max + (m_max + n_max + 7) / 8 + 1;
     ws = (ws + 31) / 32 * 32 + H2B_ACA_SLAB_PAD;  // pad: per-CTA slabs off power-of-two strides
     if (grid * ws > (int64_t)arena.n) {
       // Slabs are sized for the rank cap (min(m, n)): the top levels of dense clouds (n ~ 1e5 candidates per

@@ -460,7 +460,10 @@ void ensure_scratch(DevH2& h, int64_t R, cudaStream_t s) {
     h.wout[l].alloc(std::max<int64_t>(h.lv[l].out_total * R, 1), &h.mem);
     h.uin[l].alloc(std::max<int64_t>(h.lv[l].in_total * R, 1), &h.mem);
   }
-  if (!h.items.n) build_items(h, s);
+  // the one-directional kernel (multi-RHS chunks, non-symmetric operators) needs its work list and member
+  // tables; a symmetric operator applied to single vectors never builds them
+  const bool need_dir = !h.symmetric || R >= 16;
+  if (need_dir && !h.items.n) build_items(h, s);
   if (!h.work_counter.n) h.work_counter.alloc(1, &h.mem);
   if (h.own_in.empty()) {
     h.own_in.resize(T.depth + 1);
@@ -502,7 +505,7 @@ void ensure_scratch(DevH2& h, int64_t R, cudaStream_t s) {
   h.pack16 = RecSet();
   if (R >= 16) build_records(h, 16, s);
   if (R % 16) build_records(h, 1, s);
-  build_tabs(h, R, s);
+  if (need_dir) build_tabs(h, R, s);
   if (h.symmetric && R % 16) {
     if (!h.sym_ready) build_sym(h, s);
     build_sym_tabs(h, s);

@@ -137,6 +137,37 @@ __device__ void block_argmax(double& v, int64_t& i, RedScratch& rs) {
   i = rs.bi;
 }
 
+// argmax (non-negative candidates, ties to the lowest index) and a sum in one pass: two barriers instead of four
+template <int NT>
+__device__ double block_argmax_sum(double& v, int64_t& i, double x, RedScratch& rs) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  warp_argmax_nn(v, i);
+  x = warp_sum(x);
+  if (lane == 0) {
+    rs.v[w] = v;
+    rs.i[w] = i;
+    rs.x[w][0] = x;
+  }
+  __syncthreads();
+  if (w == 0) {
+    double v2 = lane < NW ? rs.v[lane] : -1.0;
+    int64_t i2 = lane < NW ? (int64_t)rs.i[lane] : -1;
+    warp_argmax_nn(v2, i2);
+    if (lane == 0) {
+      rs.bv = v2;
+      rs.bi = i2;
+      double s2 = 0.0;  // fixed left-to-right order over warps, as block_sum
+      for (int q = 0; q < NW; q++) s2 += rs.x[q][0];
+      rs.x[0][1] = s2;
+    }
+  }
+  __syncthreads();
+  v = rs.bv;
+  i = rs.bi;
+  return rs.x[0][1];
+}
+
 template <int NT>
 __device__ double block_sum(double x, RedScratch& rs) {
   constexpr int NW = NT / 32;
@@ -963,7 +994,13 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
         fence_proxy_async_global();  // the rows written above are read by bulk copies (async proxy) in later passes
         APROF(1);
         if (bj < 0) best = -1.0;
-        block_argmax<NT>(best, bj, rs);
+        if (fuse)  // the per-warp cross partials are complete (every batch ends with a barrier): sum them
+          for (int t = tid; t < kf; t += NT) {
+            double w = 0.0;
+            for (int q = 0; q < NW; q++) w += crosspart[q * cap + t];
+            crossv[t] = w;
+          }
+        const double v2 = block_argmax_sum<NT>(best, bj, v2p, rs);  // its barriers also publish crossv
         // The next pass (a retry with another trial row, or step k + 1) streams rows 0 .. k - 1 whatever happens:
         // start its first batches now, so they fly during the pivot search and the column pass.  (The barriers
         // inside block_argmax order every thread's row writes + proxy fence before these copies.)
@@ -972,13 +1009,7 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
           while (pre < Qn && inflight < S) issue(pre++, ki, nbn);
         }
         APROF(2);
-        if (fuse) {  // finish step k - 1: cross products, norm update, stopping test
-          for (int t = tid; t < kf; t += NT) {
-            double w = 0.0;
-            for (int q = 0; q < NW; q++) w += crosspart[q * cap + t];
-            crossv[t] = w;
-          }
-          const double v2 = block_sum<NT>(v2p, rs);  // syncs: crossv visible
+        if (fuse) {  // finish step k - 1: norm update, stopping test
           {  // every warp forms the same sum in the same order (lanes over t, then a butterfly)
             double part = 0.0;
             for (int t = lane; t < kf; t += 32) part = fma(2.0 * crossu[t], crossv[t], part);
@@ -1020,6 +1051,8 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
 #pragma unroll
       for (int q = 0; q < D; q++) yl[q] = yb[q];
       double u2p = 0.0;
+      best = -1.0;  // next trial row: the largest |u| among the unused rows, found while the column is formed
+      int64_t bi = -1;
       for (int64_t i = tid; i < m; i += NT) {
         double xl[D];
 #pragma unroll
@@ -1028,6 +1061,13 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
         for (int64_t t = 0; t < k; t++) acc = __dsub_rn(acc, __dmul_rn(U[t * m + i], vcol[t]));
         U[k * m + i] = acc;
         u2p += acc * acc;
+        if (!row_used((int)i)) {
+          const double val = fabs(acc);
+          if (val > best) {
+            best = val;
+            bi = i;
+          }
+        }
       }
       nev += m;
       __syncthreads();
@@ -1040,7 +1080,7 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
         if (lane == 0) crossu[t] = sacc;
       }
       APROF(5);
-      const double u2 = block_sum<NT>(u2p, rs);  // syncs: crossu visible
+      const double u2 = block_argmax_sum<NT>(best, bi, u2p, rs);  // syncs: crossu visible
       if (tid == 0) {
         RP[k] = trial;
         CP[k] = bj;
@@ -1059,18 +1099,6 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
         if (!(u2 * v2 <= J.eps2 * (norm2 > 0.0 ? norm2 : 0.0))) converged = 0;
         break;
       }
-      best = -1.0;
-      int64_t bi = -1;
-      const double* Uk = U + (k - 1) * m;
-      for (int64_t i = tid; i < m; i += NT)
-        if (!row_used((int)i)) {
-          const double val = fabs(Uk[i]);
-          if (val > best) {
-            best = val;
-            bi = i;
-          }
-        }
-      block_argmax<NT>(best, bi, rs);
       APROF(6);
       if (bi < 0) {  // the reference breaks after its (here irrelevant) stopping test
         finish_row((int)k - 1, false);

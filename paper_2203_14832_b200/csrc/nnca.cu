@@ -1293,6 +1293,7 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
       }
     }
   }
+  const auto wall1b = std::chrono::steady_clock::now();
   R.piv_off = upload(piv_off, s);
   R.rank.alloc(std::max<int64_t>(n, 1));
   R.conv.alloc(std::max<int64_t>(n, 1));
@@ -1316,6 +1317,10 @@ void run_side(const DevTree& T, int level, bool rows_far, const Src& own, const 
   CK(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
   CK(cudaDeviceGetAttribute(&smem_cta, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const auto wall2 = std::chrono::steady_clock::now();
+  if (getenv("H2B_SETUP_VERBOSE"))
+    fprintf(stderr, "[h2b] level %d side %d: host prep = vectors + sort %.3f ms, allocations + uploads %.3f ms\n", level,
+            which_interp, std::chrono::duration<double, std::milli>(wall1b - wall1).count(),
+            std::chrono::duration<double, std::milli>(wall2 - wall1b).count());
   CellJob J;
   J.kind = kind;
   J.a = a;

@@ -184,3 +184,24 @@ def test_reference_memory_bytes(h2c, problem):
     ops = h2.transfers[cell]
     assert ops.l2p.nbytes == 8 * cell.t_idx.size * h2.pivot_set(cell).t_in.size
     assert h2.memory_bytes() > 0
+
+
+def test_setup_is_bitwise_repeatable(h2c):
+    """The ACA kernel's work queue, prefetch ring and reductions are timing-dependent machinery; the pivots,
+    ranks, evaluation counts and interpolators it exports are not."""
+    from paper_2203_14832_b200 import sampling
+
+    pts = sampling.sphere_points(20000, 3, 5)
+    cloud = h2c.PointCloud.from_points(pts)
+    tree = h2c.build_tree(cloud, nu=64, eta=float(np.sqrt(2.0)))
+    kern = h2c.builtin_kernel("laplace-3d", 3)
+    runs = []
+    for _ in range(3):
+        h2 = h2c.assemble(tree, kern, 1e-8)
+        arrays = {(level, f): h2.array(level, f).copy() for level in h2.compressed_levels()
+                  for f in ("k_in", "t_in", "s_in", "nevals", "converged")}
+        cell = tree.nonempty_cells(tree.depth - 1)[3]
+        runs.append((arrays, h2.interp(cell.level, cell._ref_index, 0)))
+    for arrays, P in runs[1:]:
+        assert all(np.array_equal(arrays[k], runs[0][0][k]) for k in arrays)
+        assert np.array_equal(P, runs[0][1])

@@ -1,6 +1,7 @@
 // nnca.cu — NNCA construction on the GPU (compress.py:216 select_pivots,
 // compress.py:285 assemble) with the partially pivoted ACA of
-// _accel/_core.pyx:70 run as one CTA per cell, level-batched bottom-up.
+// _accel/_core.pyx:70 run by persistent CTAs (one cell at a time each, cells
+// pulled from a work queue), level-batched bottom-up.
 //
 // Pivot parity: every residual entry is formed with the reference's exact
 // operation order (kernel value, then `acc -= U[i,t] * V[j,t]` for t =
@@ -547,8 +548,8 @@ DBuf<T> upload(const std::vector<T>& h, cudaStream_t s, MemStats* ms = nullptr) 
 // Persistent level-batched ACA (the setup hot path).
 //
 // CTAs pull cells from a work queue (largest first).  A CTA's workspace (the
-// residual factors U, V, the gathered far candidates, used-row/column flags)
-// is a fixed per-CTA slab reused cell after cell.  Pivot arithmetic is the
+// residual factors U, V, the positions of the far candidates in the level's
+// source arrays) is a fixed per-CTA slab reused cell after cell.  Pivot arithmetic is the
 // reference's (see aca_kernel): every residual entry is
 //     K(x_i, y_j) - U[i,0] V[j,0] - ... - U[i,k-1] V[j,k-1]
 // rounded after every multiply and every subtract, left to right.
@@ -556,11 +557,12 @@ DBuf<T> upload(const std::vector<T>& h, cudaStream_t s, MemStats* ms = nullptr) 
 // Row pass (the hot loop: step k re-reads all k previous residual rows):
 // one thread owns NC columns of a column segment and keeps their running
 // entries in registers, while the previous rows V[t][segment] stream through
-// a two-slot shared-memory ring of TB rows each, filled by TMA bulk copies
+// an S-slot shared-memory ring of TB rows each, filled by TMA bulk copies
 // (cp.async.bulk, mbarrier completion; one copy per row, issued by thread 0
-// two batches ahead).  The copies keep TB rows x segment bytes in flight per
-// slot with no registers held, which is what the latency-bound register
-// version lacked (ncu: 16 warps, long-scoreboard stalls, 1.2 TB/s).  The
+// S - 1 batches ahead, across segment and pass boundaries).  The copies keep
+// TB rows x segment bytes in flight per slot with no registers held, which is
+// what the latency-bound register version lacked (ncu: 16 warps,
+// long-scoreboard stalls, 1.2 TB/s).  The
 // pass also finishes step k - 1 (normalises its raw row, forms the cross
 // products <V[t], V[k-1]> for the stopping test) so V is swept once per step.
 // Kernel families (1/r-like, exp, log) are separate instantiations: the

@@ -1006,7 +1006,7 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
         // The next pass (a retry with another trial row, or step k + 1) streams rows 0 .. k - 1 whatever happens:
         // start its first batches now, so they fly during the pivot search and the column pass.  (The barriers
         // inside block_argmax order every thread's row writes + proxy fence before these copies.)
-        if (ki > 0) {
+        if (ki > 0 && !(best > 0.0 && k + 1 == full)) {  // (the last step of a cell is followed by no pass)
           const int nbn = (ki + TB - 1) / TB, Qn = nseg * nbn;
           while (pre < Qn && inflight < S) issue(pre++, ki, nbn);
         }
@@ -1039,6 +1039,19 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
         __syncthreads();
       }
       if (stop_prev || exhausted) break;
+      if (WHICH == 0 && k + 1 == full && full == m) {
+        // Last step of a cell whose rank reaches its row count (most leaves): the reference stops at k == full
+        // whatever the stopping test says, every row is then a pivot row, so the interpolator is a permutation
+        // and neither the last residual column nor the normalised last row is ever read.  Only the column pivot
+        // found above and the evaluation count of the skipped column pass are recorded.
+        if (tid == 0) {
+          RP[k] = trial;
+          CP[k] = bj;
+        }
+        nev += m;
+        k += 1;
+        break;
+      }
       // pivot of step k; the row stays raw until the next pass normalises it
       const double piv = V[k * ldv + bj];
       if (tid < D) yb[tid] = colc(tid, bj);

@@ -1187,11 +1187,9 @@ __global__ void __launch_bounds__(NT, MB) aca_ring(CellJob J) {
 
 template <int D, int NT>
 void set_aca_smem(size_t bytes) {
-  static size_t done = 0;
-  if (bytes > 40 * 1024 && bytes > done) {
+  // the attribute is per device: set on every call that needs the opt-in (a process may drive several GPUs)
+  if (bytes > 40 * 1024)
     CK(cudaFuncSetAttribute(aca_kernel<D, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    done = bytes;
-  }
 }
 
 // One side (incoming or outgoing) of the NNCA for one level.
